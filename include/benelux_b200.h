@@ -1,0 +1,140 @@
+/*
+ * benelux_b200.h -- C ABI of the B200-native Benelux-pair search (libbenelux_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures (a stream is
+ * passed as an opaque `void*` holding a cudaStream_t, 0 = the library's own stream).
+ * Host pointers unless a name ends in `_dev`.  Every entry point returns a status code.
+ *
+ * Each entry point replaces one seam of the reference package `benelux_pairs`
+ * (paths relative to /root/reference/pkg/src/benelux_pairs/):
+ *
+ *   bnx_primes_up_to            <- primes.py:24-35           primes_up_to(limit)
+ *   bnx_sieve_radicals          <- radical.py:109-124 +      sieve_radicals(Interval, PrimeList,
+ *                                  _kernels.py:22-84           ctz_fast_path) / sieve_segment
+ *   bnx_radicals_trial_division <- _kernels.py:87-112        radicals_trial_division(start, length)
+ *   bnx_search                  <- sort_search.py:37-91      find_pairs_sorted(limit, primes)
+ *   bnx_search_domain           <- chunked.py:307-359        search_chunk(index, s, primes, n_limit)
+ *                                  (+ chunked.py:362-412      run_full_chunked, one call per chunk)
+ *   bnx_slot_of                 <- _kernels.py:115-123 /     _slot_of / commutative_hash
+ *                                  chunked.py:93-109
+ *   status codes                <- _kernels.py:17-19         STATUS_OK / TABLE_FULL / BUFFER_FULL
+ *
+ * Error convention (mirrors _kernels.py:17-19 and the front-ends' exceptions):
+ *   BNX_OK                   0  success
+ *   BNX_TABLE_FULL           1  (reserved; TableFullError)
+ *   BNX_BUFFER_FULL          2  `cap` too small: *found holds the required count; the
+ *                               caller grows the buffer and calls again (chunked.py:268-270)
+ *   BNX_ERR_PRIMES_UNCOVERED 3  supplied primes do not reach isqrt(endpoint) -> ValueError
+ *                               (radical.py:119-120)
+ *   BNX_ERR_INVALID          4  bad argument (limit < 3, empty interval, ...) -> ValueError
+ *   BNX_ERR_CUDA             5  CUDA runtime failure / no device           -> RuntimeError
+ *   BNX_ERR_RANGE            6  bound beyond this build's exact range (S >= 2^42)
+ *   bnx_last_error() gives a message for the most recent failure on the calling thread.
+ */
+#ifndef BENELUX_B200_H
+#define BENELUX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BNX_API __attribute__((visibility("default")))
+#else
+#define BNX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BNX_OK 0
+#define BNX_TABLE_FULL 1
+#define BNX_BUFFER_FULL 2
+#define BNX_ERR_PRIMES_UNCOVERED 3
+#define BNX_ERR_INVALID 4
+#define BNX_ERR_CUDA 5
+#define BNX_ERR_RANGE 6
+
+#define BNX_KIND_FIRST 1u  /* signatures.py:14-16 Kind.FIRST  */
+#define BNX_KIND_SECOND 2u /* signatures.py:14-16 Kind.SECOND */
+#define BNX_KIND_BOTH 3u
+
+/* One result row: BeneluxPair (signatures.py:48-64) / CLI row kind,m,n,rad_m,rad_m1
+ * (cli.py:111-125).  rad_m, rad_m1 are rad(m), rad(m+1) in natural order. */
+typedef struct bnx_pair {
+    uint64_t m;
+    uint64_t n;
+    uint64_t rad_m;
+    uint64_t rad_m1;
+    int32_t kind; /* 1 first, 2 second */
+    int32_t reserved;
+} bnx_pair_t;
+
+/* Per-call counters of the last search (diagnostics and bench). */
+typedef struct bnx_stats {
+    uint64_t integers;       /* n values examined by the screen                      */
+    uint64_t survivors;      /* n passing the on-chip log-surplus screen              */
+    uint64_t candidates;     /* n with rad(n)*rad(n+1) <= 2n (exact)                  */
+    uint64_t residue_checks; /* m values enumerated on the residue classes            */
+    uint64_t matches;        /* (m, n) with equal signatures                          */
+    uint64_t pairs;          /* rows emitted after the kind filter                    */
+    uint64_t kernel_launches;/* kernels this library launched for the call            */
+    int32_t bucket_overflow; /* nonzero if a tile bucket overflowed (call failed)     */
+    int32_t reserved;
+} bnx_stats_t;
+
+typedef struct bnx_ctx bnx_ctx_t;
+
+BNX_API int bnx_version(void);
+BNX_API const char* bnx_last_error(void);
+BNX_API int bnx_device_count(int* count);
+
+/* Context: one GPU, one stream, cached prime tables and work buffers. */
+BNX_API int bnx_ctx_create(int device, bnx_ctx_t** out);
+BNX_API int bnx_ctx_destroy(bnx_ctx_t* ctx);
+BNX_API int bnx_ctx_set_stream(bnx_ctx_t* ctx, void* stream);
+BNX_API int bnx_ctx_stats(const bnx_ctx_t* ctx, bnx_stats_t* out);
+
+/* primes.py:24-35: all primes <= limit, ascending.  *count always receives the total;
+ * BNX_BUFFER_FULL if it exceeds cap. */
+BNX_API int bnx_primes_up_to(bnx_ctx_t* ctx, uint64_t limit, uint64_t* out, size_t cap, size_t* count);
+
+/* radical.py:109-124: out[k] = rad(start + k), k < length.  `primes` (ascending, covering
+ * `primes_limit` = PrimeList.limit) may be NULL to let the device build them.  Returns
+ * BNX_ERR_PRIMES_UNCOVERED when primes_limit < isqrt(start + length - 1). */
+BNX_API int bnx_sieve_radicals(bnx_ctx_t* ctx, uint64_t start, uint64_t length, const uint64_t* primes,
+                       size_t nprimes, uint64_t primes_limit, int ctz_fast_path, uint64_t* out);
+/* Same, writing into device memory `out_dev` on the context stream (no host sync). */
+BNX_API int bnx_sieve_radicals_dev(bnx_ctx_t* ctx, uint64_t start, uint64_t length, int ctz_fast_path,
+                           uint64_t* out_dev);
+
+/* _kernels.py:87-112: out[k] = rad(start + k) by per-integer trial division on the GPU. */
+BNX_API int bnx_radicals_trial_division(bnx_ctx_t* ctx, uint64_t start, uint64_t length, uint64_t* out);
+
+/* sort_search.py:37-91: every pair m < n < limit of the kinds in kinds_mask.
+ * Rows come back sorted by (m, n).  primes may be NULL (device-built). */
+BNX_API int bnx_search(bnx_ctx_t* ctx, uint64_t limit, uint32_t kinds_mask, const uint64_t* primes,
+               size_t nprimes, uint64_t primes_limit, bnx_pair_t* out, size_t cap, size_t* found);
+
+/* chunked.py:307-359: every pair (m, n), m < n, with n_first <= n <= n_last (any m >= 1).
+ * Rows sorted by (n, m) (chunked.py:358). */
+BNX_API int bnx_search_domain(bnx_ctx_t* ctx, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask,
+                      const uint64_t* primes, size_t nprimes, uint64_t primes_limit, bnx_pair_t* out,
+                      size_t cap, size_t* found);
+
+/* Split-phase form for timing: enqueue the whole search on the context stream without a
+ * host sync (device-resident prime tables must already exist: call bnx_prepare first),
+ * then collect.  bnx_prepare builds / uploads the tables for bound `max_x`. */
+BNX_API int bnx_prepare(bnx_ctx_t* ctx, uint64_t max_x, const uint64_t* primes, size_t nprimes,
+                uint64_t primes_limit);
+BNX_API int bnx_search_enqueue(bnx_ctx_t* ctx, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask);
+BNX_API int bnx_search_collect(bnx_ctx_t* ctx, bnx_pair_t* out, size_t cap, size_t* found);
+
+/* _kernels.py:115-123: the reference's commutative slot hash (host, for API parity). */
+BNX_API uint64_t bnx_slot_of(uint64_t lo, uint64_t hi, uint64_t mask, uint64_t phi, uint64_t mul1, uint64_t mul2);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BENELUX_B200_H */

@@ -1,0 +1,593 @@
+// bnx_capi.cu -- host runtime and C ABI (include/benelux_b200.h) of libbenelux_b200.so.
+//
+// One context = one GPU + one stream + cached device tables (primes, prime-power
+// progressions, exact-division constants) + work buffers reused across calls.  All device
+// work of a search is enqueued back to back on the context stream; the host synchronises
+// once to read the counters and the (tiny) pair list.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/benelux_b200.h"
+#include "bnx_kernels.cuh"
+
+using namespace bnx;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) return fail(BNX_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define TRY(call)                   \
+    do {                            \
+        int r_ = (call);            \
+        if (r_ != BNX_OK) return r_; \
+    } while (0)
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t n) {
+        if (n <= cap && p) return BNX_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n, 1);
+        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+        if (e != cudaSuccess) return fail(BNX_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        cap = want;
+        return BNX_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+uint64_t isqrt_u64(uint64_t x) {
+    uint64_t r = (uint64_t)std::sqrt((long double)x);
+    while (r > 0 && (r > 0xFFFFFFFFull || r * r > x)) --r;
+    while (r + 1 <= 0xFFFFFFFFull && (r + 1) * (r + 1) <= x) ++r;
+    return r;
+}
+
+uint64_t icbrt_u64(uint64_t x) {
+    uint64_t r = (uint64_t)std::cbrt((long double)x);
+    auto cube_le = [&](uint64_t v) { return v <= 2642245ull && v * v * v <= x; };
+    while (r > 0 && !cube_le(r)) --r;
+    while (cube_le(r + 1)) ++r;
+    return r;
+}
+
+struct Tables {
+    uint64_t max_x = 0;
+    int include_two = -1;
+    uint32_t tile = 0;
+    uint64_t gen = ~0ull;
+    DBuf<BnxProg> small, large;
+    DBuf<BnxPDiv> pdiv;
+    uint32_t nsmall = 0;
+    uint64_t nlarge = 0, npdiv = 0;
+    void release() {
+        small.release();
+        large.release();
+        pdiv.release();
+        gen = ~0ull;
+    }
+};
+
+}  // namespace
+
+struct bnx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    int screen_blocks_per_sm = 1;
+    int sieve_blocks_per_sm = 1;
+
+    // prime table (device u32 + host mirror)
+    DBuf<uint32_t> primes;
+    std::vector<uint32_t> h_primes;
+    uint64_t primes_limit = 0;  // PrimeList.limit the table covers
+    uint64_t gen = 0;           // bumps whenever the table changes
+    DBuf<uint64_t> stage64;
+
+    Tables screen_tab, sieve_tab, td_tab;
+
+    DBuf<uint64_t> surv;
+    DBuf<BnxCand> cand;
+    DBuf<BnxMatch> match;
+    DBuf<bnx_pair_t> pairs;
+    DBuf<unsigned long long> ctr;
+    DBuf<int> flags;
+    unsigned long long* h_ctr = nullptr;
+    int* h_flags = nullptr;
+
+    DBuf<uint32_t> t_nsmall;
+    DBuf<unsigned long long> t_nlarge;
+    DBuf<uint64_t> t_npdiv;
+    DBuf<int> t_over;
+    DBuf<uint64_t> sieve_out;
+
+    // the enqueued search
+    bool q_valid = false;
+    uint64_t q_first = 0, q_last = 0;
+    uint32_t q_kinds = 0;
+    bnx_stats_t stats{};
+};
+
+namespace {
+
+int activate(bnx_ctx* c) {
+    CK(cudaSetDevice(c->device));
+    return BNX_OK;
+}
+
+// Device Eratosthenes up to `limit` (< 2^32): base primes by one block, then a segmented
+// pass (count, scan, write).  Replaces the table; host mirror refreshed.
+int gen_primes(bnx_ctx* c, uint64_t limit) {
+    if (limit >= (1ull << 32)) return fail(BNX_ERR_RANGE, "prime tables are limited to < 2^32");
+    if (limit < 2) limit = 2;
+    const uint32_t ls = (uint32_t)std::min<uint64_t>(limit, (uint64_t)std::max<uint64_t>(isqrt_u64(limit), 2));
+    DBuf<uint32_t> base, cnt;
+    TRY(base.ensure(ls / 2 + 16));
+    TRY(cnt.ensure(1));
+    launch_base_primes(ls, base.p, cnt.p, c->stream);
+    CK(cudaGetLastError());
+    uint32_t nbase = 0;
+    CK(cudaMemcpyAsync(&nbase, cnt.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    uint64_t total = 0;
+    if (limit <= ls) {
+        TRY(c->primes.ensure(nbase));
+        CK(cudaMemcpyAsync(c->primes.p, base.p, sizeof(uint32_t) * nbase, cudaMemcpyDeviceToDevice, c->stream));
+        total = nbase;
+    } else {
+        const uint64_t nblocks = (limit + 1 + 32767) / 32768;
+        DBuf<uint32_t> counts;
+        DBuf<uint64_t> offs;
+        TRY(counts.ensure(nblocks));
+        TRY(offs.ensure(nblocks + 1));
+        launch_prime_seg(0, limit, base.p, nbase, counts.p, nullptr, nullptr, nblocks, c->stream);
+        launch_scan_counts(counts.p, nblocks, 0, offs.p, c->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&total, offs.p + nblocks, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        TRY(c->primes.ensure(total));
+        launch_prime_seg(0, limit, base.p, nbase, counts.p, offs.p, c->primes.p, nblocks, c->stream);
+        CK(cudaGetLastError());
+        counts.release();
+        offs.release();
+    }
+    c->h_primes.resize(total);
+    CK(cudaMemcpyAsync(c->h_primes.data(), c->primes.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    base.release();
+    cnt.release();
+    c->primes_limit = limit;
+    c->gen++;
+    return BNX_OK;
+}
+
+// Caller-supplied PrimeList (host, ascending, uint64): checked for coverage, the primes up to
+// `need` are copied to the device.
+int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes_limit, uint64_t need) {
+    if (primes_limit < need)
+        return fail(BNX_ERR_PRIMES_UNCOVERED, "prime list covers " + std::to_string(primes_limit) +
+                                                  " but interval endpoint needs " + std::to_string(need));
+    size_t k = (size_t)(std::upper_bound(primes, primes + np, need) - primes);
+    TRY(c->stage64.ensure(k));
+    TRY(c->primes.ensure(k));
+    if (k) {
+        CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->stream));
+        launch_narrow(c->stage64.p, k, c->primes.p, c->stream);
+        CK(cudaGetLastError());
+    }
+    c->h_primes.resize(k);
+    for (size_t i = 0; i < k; ++i) c->h_primes[i] = (uint32_t)primes[i];
+    c->primes_limit = need;  // the device copy holds exactly the primes <= need
+    c->gen++;
+    return BNX_OK;
+}
+
+int ensure_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes_limit, uint64_t need) {
+    if (primes) return upload_primes(c, primes, np, primes_limit, need);
+    if (c->gen > 0 && c->primes_limit >= need) return BNX_OK;
+    uint64_t lim = std::max<uint64_t>(need, 65536);
+    if (lim >= (1ull << 32)) lim = (1ull << 32) - 1;
+    return gen_primes(c, lim);
+}
+
+int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_t tile) {
+    if (t.gen == c->gen && t.max_x == max_x && t.include_two == include_two && t.tile == tile) return BNX_OK;
+    const uint64_t root = isqrt_u64(max_x);
+    const uint64_t np = (uint64_t)(std::upper_bound(c->h_primes.begin(), c->h_primes.end(), (uint32_t)std::min<uint64_t>(root, 0xFFFFFFFFull)) - c->h_primes.begin());
+    const uint64_t cb = icbrt_u64(max_x);
+    const uint64_t npc = (uint64_t)(std::upper_bound(c->h_primes.begin(), c->h_primes.end(), (uint32_t)std::min<uint64_t>(cb, 0xFFFFFFFFull)) - c->h_primes.begin());
+    const uint64_t large_cap = np + 63 * npc + 64;
+    const uint32_t small_cap = (uint32_t)(tile == (uint32_t)SCREEN_TILE ? SCREEN_MAXS : SIEVE_MAXS);
+    TRY(t.small.ensure(small_cap));
+    TRY(t.large.ensure(large_cap));
+    TRY(t.pdiv.ensure(np + 1));
+    TRY(c->t_nsmall.ensure(1));
+    TRY(c->t_nlarge.ensure(1));
+    TRY(c->t_npdiv.ensure(1));
+    TRY(c->t_over.ensure(1));
+    CK(cudaMemsetAsync(c->t_nsmall.p, 0, sizeof(uint32_t), c->stream));
+    CK(cudaMemsetAsync(c->t_nlarge.p, 0, sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->t_npdiv.p, 0, sizeof(uint64_t), c->stream));
+    CK(cudaMemsetAsync(c->t_over.p, 0, sizeof(int), c->stream));
+    if (np) {
+        launch_build_tables(c->primes.p, np, max_x, include_two, tile, t.small.p, c->t_nsmall.p, small_cap, t.large.p,
+                            c->t_nlarge.p, large_cap, t.pdiv.p, c->t_npdiv.p, c->t_over.p, c->stream);
+        CK(cudaGetLastError());
+    }
+    uint32_t ns = 0;
+    unsigned long long nl = 0;
+    uint64_t npd = 0;
+    int over = 0;
+    CK(cudaMemcpyAsync(&ns, c->t_nsmall.p, sizeof(ns), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&nl, c->t_nlarge.p, sizeof(nl), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&npd, c->t_npdiv.p, sizeof(npd), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&over, c->t_over.p, sizeof(over), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (over) return fail(BNX_ERR_CUDA, "progression table overflow");
+    t.nsmall = ns;
+    t.nlarge = nl;
+    t.npdiv = npd;
+    t.max_x = max_x;
+    t.include_two = include_two;
+    t.tile = tile;
+    t.gen = c->gen;
+    return BNX_OK;
+}
+
+int ensure_work(bnx_ctx* c) {
+    if (!c->surv.p) TRY(c->surv.ensure(1 << 20));
+    if (!c->cand.p) TRY(c->cand.ensure(1 << 16));
+    if (!c->match.p) TRY(c->match.ensure(1 << 16));
+    if (!c->pairs.p) TRY(c->pairs.ensure(1 << 14));
+    TRY(c->ctr.ensure(CTR_N));
+    TRY(c->flags.ensure(4));
+    if (!c->h_ctr) CK(cudaMallocHost(&c->h_ctr, sizeof(unsigned long long) * CTR_N));
+    if (!c->h_flags) CK(cudaMallocHost(&c->h_flags, sizeof(int) * 4));
+    return BNX_OK;
+}
+
+int grid_for(bnx_ctx* c) { return c->num_sms * 4; }
+
+int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
+    Tables& t = c->screen_tab;
+    TRY(ensure_work(c));
+    const uint64_t SEG = (uint64_t)SCREEN_TILE * SCREEN_NT;
+    const uint64_t x_begin = n_first / SCREEN_TILE * SCREEN_TILE;
+    const uint64_t nseg = (n_last - x_begin + 1 + SEG - 1) / SEG;
+    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+    CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+    ScreenArgs sa{x_begin, nseg, n_first, n_last, t.small.p, (int)t.nsmall, t.large.p, (int)t.nlarge,
+                  c->surv.p, c->surv.cap, c->ctr.p, c->flags.p};
+    const int sgrid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->screen_blocks_per_sm);
+    launch_screen(sa, sgrid, c->stream);
+    VerifyArgs va{c->surv.p, c->surv.cap, t.pdiv.p, t.npdiv, c->cand.p, c->cand.cap, c->ctr.p};
+    launch_verify(va, grid_for(c), c->stream);
+    EnumArgs ea{c->cand.p, c->cand.cap, kinds, c->match.p, c->match.cap, c->ctr.p};
+    launch_enumerate(ea, grid_for(c), c->stream);
+    FinalArgs fa{c->match.p, c->match.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap, c->ctr.p};
+    launch_finalize(fa, grid_for(c), c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    c->q_valid = true;
+    c->q_first = n_first;
+    c->q_last = n_last;
+    c->q_kinds = kinds;
+    c->stats = bnx_stats_t{};
+    c->stats.integers = n_last - n_first + 1;
+    c->stats.kernel_launches = 4;
+    return BNX_OK;
+}
+
+int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint64_t plimit) {
+    if (max_x >= (1ull << 42)) return fail(BNX_ERR_RANGE, "search bound must be below 2^42");
+    const uint64_t need = isqrt_u64(max_x);
+    TRY(ensure_primes(c, primes, np, plimit, need));
+    TRY(build_tables(c, c->screen_tab, max_x, 0, SCREEN_TILE));
+    if (c->screen_tab.nsmall > (uint32_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
+    return BNX_OK;
+}
+
+// Sync, grow-and-retry on any capacity overflow, copy the pair list out.
+int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
+    if (!c->q_valid) return fail(BNX_ERR_INVALID, "no search enqueued");
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->h_flags[0]) return fail(BNX_ERR_CUDA, "screen bucket overflow");
+        const unsigned long long* h = c->h_ctr;
+        bool again = false;
+        if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
+        if (h[CTR_CAND] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_CAND] * 2)); again = true; }
+        if (h[CTR_MATCH] > c->match.cap) { TRY(c->match.ensure(h[CTR_MATCH] * 2)); again = true; }
+        if (h[CTR_PAIRS] > c->pairs.cap) { TRY(c->pairs.ensure(h[CTR_PAIRS] * 2)); again = true; }
+        if (again) {
+            TRY(enqueue(c, c->q_first, c->q_last, c->q_kinds));
+            continue;
+        }
+        const uint64_t np = h[CTR_PAIRS];
+        rows.resize(np);
+        if (np) {
+            CK(cudaMemcpyAsync(rows.data(), c->pairs.p, sizeof(bnx_pair_t) * np, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        c->stats.survivors = h[CTR_SURV];
+        c->stats.candidates = h[CTR_CAND];
+        c->stats.residue_checks = h[CTR_CHECKS];
+        c->stats.matches = h[CTR_MATCH];
+        c->stats.pairs = np;
+        c->q_valid = false;
+        return BNX_OK;
+    }
+    return fail(BNX_ERR_CUDA, "capacity retries exhausted");
+}
+
+int emit(const std::vector<bnx_pair_t>& rows, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (found) *found = rows.size();
+    if (rows.size() > cap) return fail(BNX_BUFFER_FULL, "pair buffer too small");
+    if (out && !rows.empty()) std::memcpy(out, rows.data(), rows.size() * sizeof(bnx_pair_t));
+    return BNX_OK;
+}
+
+int search_rows(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds, const uint64_t* primes, size_t np,
+                uint64_t plimit, std::vector<bnx_pair_t>& rows) {
+    if (n_first < 1 || n_last < n_first) return fail(BNX_ERR_INVALID, "empty search domain");
+    if ((kinds & 3u) == 0) return fail(BNX_ERR_INVALID, "kinds_mask selects no kind");
+    TRY(activate(c));
+    TRY(prepare(c, n_last + 1, primes, np, plimit));
+    TRY(enqueue(c, n_first, n_last, kinds & 3u));
+    return collect(c, rows);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bnx_version(void) { return 10000; }
+
+const char* bnx_last_error(void) { return g_err.c_str(); }
+
+int bnx_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    if (count) *count = n;
+    return n > 0 ? BNX_OK : fail(BNX_ERR_CUDA, "no CUDA device");
+}
+
+int bnx_ctx_create(int device, bnx_ctx_t** out) {
+    if (!out) return fail(BNX_ERR_INVALID, "null out");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(BNX_ERR_CUDA, "no CUDA device");
+    if (device < 0 || device >= n) return fail(BNX_ERR_INVALID, "bad device index");
+    bnx_ctx* c = new bnx_ctx();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaFuncSetAttribute(screen_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_smem_bytes()));
+    CK(cudaFuncSetAttribute(sieve_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sieve_smem_bytes()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->screen_blocks_per_sm, screen_kernel(), SCREEN_THREADS,
+                                                     screen_smem_bytes()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_blocks_per_sm, sieve_kernel(), SIEVE_THREADS,
+                                                     sieve_smem_bytes()));
+    c->screen_blocks_per_sm = std::max(1, c->screen_blocks_per_sm);
+    c->sieve_blocks_per_sm = std::max(1, c->sieve_blocks_per_sm);
+    *out = c;
+    return BNX_OK;
+}
+
+int bnx_ctx_destroy(bnx_ctx_t* c) {
+    if (!c) return BNX_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    c->primes.release();
+    c->stage64.release();
+    c->screen_tab.release();
+    c->sieve_tab.release();
+    c->td_tab.release();
+    c->surv.release();
+    c->cand.release();
+    c->match.release();
+    c->pairs.release();
+    c->ctr.release();
+    c->flags.release();
+    c->t_nsmall.release();
+    c->t_nlarge.release();
+    c->t_npdiv.release();
+    c->t_over.release();
+    c->sieve_out.release();
+    if (c->h_ctr) cudaFreeHost(c->h_ctr);
+    if (c->h_flags) cudaFreeHost(c->h_flags);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return BNX_OK;
+}
+
+int bnx_ctx_set_stream(bnx_ctx_t* c, void* stream) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    TRY(activate(c));
+    if (c->own_stream && c->stream) {
+        cudaStreamSynchronize(c->stream);
+        cudaStreamDestroy(c->stream);
+    }
+    if (stream) {
+        c->stream = (cudaStream_t)stream;
+        c->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    return BNX_OK;
+}
+
+int bnx_ctx_stats(const bnx_ctx_t* c, bnx_stats_t* out) {
+    if (!c || !out) return fail(BNX_ERR_INVALID, "null argument");
+    *out = c->stats;
+    return BNX_OK;
+}
+
+int bnx_primes_up_to(bnx_ctx_t* c, uint64_t limit, uint64_t* out, size_t cap, size_t* count) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (count) *count = 0;
+    if (limit < 2) return BNX_OK;
+    TRY(activate(c));
+    TRY(gen_primes(c, limit));
+    const size_t n = c->h_primes.size();
+    if (count) *count = n;
+    if (n > cap) return fail(BNX_BUFFER_FULL, "prime buffer too small");
+    for (size_t i = 0; i < n; ++i) out[i] = c->h_primes[i];
+    return BNX_OK;
+}
+
+static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint64_t* primes, size_t np,
+                        uint64_t plimit, int fast, uint64_t* out_host, uint64_t* out_dev) {
+    if (start < 1) return fail(BNX_ERR_INVALID, "interval must start at 1 or above");
+    if (length < 1) return fail(BNX_ERR_INVALID, "interval length must be >= 1");
+    if (length - 1 > ~0ull - start) return fail(BNX_ERR_INVALID, "interval endpoint exceeds 64 bits");
+    TRY(activate(c));
+    const uint64_t end = start + (length - 1);
+    const uint64_t need = isqrt_u64(end);
+    TRY(ensure_primes(c, primes, np, plimit, need));
+    TRY(build_tables(c, c->sieve_tab, end, fast ? 0 : 1, SIEVE_TILE));
+    if (c->sieve_tab.nsmall > (uint32_t)SIEVE_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
+    TRY(c->flags.ensure(4));
+    if (!c->h_flags) CK(cudaMallocHost(&c->h_flags, sizeof(int) * 4));
+    CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+    const uint64_t piece = out_dev ? length : std::min<uint64_t>(length, 1ull << 27);
+    if (!out_dev) TRY(c->sieve_out.ensure(piece));
+    const uint64_t SEG = (uint64_t)SIEVE_TILE * SIEVE_NT;
+    for (uint64_t off = 0; off < length; off += piece) {
+        const uint64_t len = std::min<uint64_t>(piece, length - off);
+        uint64_t* dst = out_dev ? out_dev : c->sieve_out.p;
+        SieveArgs sa{start + off, len, c->sieve_tab.small.p, (int)c->sieve_tab.nsmall, c->sieve_tab.large.p,
+                     c->sieve_tab.nlarge, fast, dst, c->flags.p};
+        const uint64_t nseg = (len + SEG - 1) / SEG;
+        const int grid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->sieve_blocks_per_sm);
+        launch_sieve(sa, grid, c->stream);
+        CK(cudaGetLastError());
+        if (!out_dev) CK(cudaMemcpyAsync(out_host + off, dst, sizeof(uint64_t) * len, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->h_flags[0]) return fail(BNX_ERR_CUDA, "sieve bucket overflow");
+    return BNX_OK;
+}
+
+int bnx_sieve_radicals(bnx_ctx_t* c, uint64_t start, uint64_t length, const uint64_t* primes, size_t nprimes,
+                       uint64_t primes_limit, int ctz_fast_path, uint64_t* out) {
+    if (!c || !out) return fail(BNX_ERR_INVALID, "null argument");
+    return sieve_common(c, start, length, primes, nprimes, primes_limit, ctz_fast_path, out, nullptr);
+}
+
+int bnx_sieve_radicals_dev(bnx_ctx_t* c, uint64_t start, uint64_t length, int ctz_fast_path, uint64_t* out_dev) {
+    if (!c || !out_dev) return fail(BNX_ERR_INVALID, "null argument");
+    return sieve_common(c, start, length, nullptr, 0, 0, ctz_fast_path, nullptr, out_dev);
+}
+
+int bnx_radicals_trial_division(bnx_ctx_t* c, uint64_t start, uint64_t length, uint64_t* out) {
+    if (!c || !out) return fail(BNX_ERR_INVALID, "null argument");
+    if (start < 1) return fail(BNX_ERR_INVALID, "interval must start at 1 or above");
+    if (length < 1) return fail(BNX_ERR_INVALID, "interval length must be >= 1");
+    if (length - 1 > ~0ull - start) return fail(BNX_ERR_INVALID, "interval endpoint exceeds 64 bits");
+    TRY(activate(c));
+    const uint64_t end = start + (length - 1);
+    TRY(ensure_primes(c, nullptr, 0, 0, isqrt_u64(end)));
+    TRY(build_tables(c, c->td_tab, end, 0, SIEVE_TILE));
+    const uint64_t piece = std::min<uint64_t>(length, 1ull << 26);
+    TRY(c->sieve_out.ensure(piece));
+    for (uint64_t off = 0; off < length; off += piece) {
+        const uint64_t len = std::min<uint64_t>(piece, length - off);
+        launch_trial_division(start + off, len, c->td_tab.pdiv.p, c->td_tab.npdiv, c->sieve_out.p, c->num_sms * 8,
+                              c->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out + off, c->sieve_out.p, sizeof(uint64_t) * len, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return BNX_OK;
+}
+
+int bnx_prepare(bnx_ctx_t* c, uint64_t max_x, const uint64_t* primes, size_t nprimes, uint64_t primes_limit) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    TRY(activate(c));
+    return prepare(c, max_x, primes, nprimes, primes_limit);
+}
+
+int bnx_search_enqueue(bnx_ctx_t* c, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (n_first < 1 || n_last < n_first) return fail(BNX_ERR_INVALID, "empty search domain");
+    if (c->screen_tab.gen != c->gen || c->screen_tab.max_x < n_last + 1)
+        return fail(BNX_ERR_INVALID, "bnx_prepare must cover n_last + 1 first");
+    TRY(activate(c));
+    return enqueue(c, n_first, n_last, kinds_mask & 3u);
+}
+
+int bnx_search_collect(bnx_ctx_t* c, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    TRY(activate(c));
+    std::vector<bnx_pair_t> rows;
+    TRY(collect(c, rows));
+    std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
+        return a.n != b.n ? a.n < b.n : a.m < b.m;
+    });
+    return emit(rows, out, cap, found);
+}
+
+int bnx_search(bnx_ctx_t* c, uint64_t limit, uint32_t kinds_mask, const uint64_t* primes, size_t nprimes,
+               uint64_t primes_limit, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (limit < 3) return fail(BNX_ERR_INVALID, "limit must be >= 3");
+    std::vector<bnx_pair_t> rows;
+    TRY(search_rows(c, 1, limit - 1, kinds_mask, primes, nprimes, primes_limit, rows));
+    std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
+        return a.m != b.m ? a.m < b.m : a.n < b.n;
+    });
+    return emit(rows, out, cap, found);
+}
+
+int bnx_search_domain(bnx_ctx_t* c, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask, const uint64_t* primes,
+                      size_t nprimes, uint64_t primes_limit, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    std::vector<bnx_pair_t> rows;
+    TRY(search_rows(c, n_first, n_last, kinds_mask, primes, nprimes, primes_limit, rows));
+    std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
+        return a.n != b.n ? a.n < b.n : a.m < b.m;
+    });
+    return emit(rows, out, cap, found);
+}
+
+uint64_t bnx_slot_of(uint64_t lo, uint64_t hi, uint64_t mask, uint64_t phi, uint64_t mul1, uint64_t mul2) {
+    uint64_t x = lo ^ (hi * phi);
+    x = (x ^ (x >> 30)) * mul1;
+    x = (x ^ (x >> 27)) * mul2;
+    x = x ^ (x >> 31);
+    return x & mask;
+}
+
+}  // extern "C"

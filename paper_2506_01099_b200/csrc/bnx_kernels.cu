@@ -1,0 +1,604 @@
+// bnx_kernels.cu -- sm_100a kernels of the B200-native Benelux-pair search.
+//
+// Hot path:
+//   k_screen        on-chip segmented sieve of the quarter-bit log of the "surplus"
+//                   s(x) = x / rad(x) over shared-memory tiles; flags every n whose
+//                   signature could collide:  rad(n) * rad(n+1) <= 2n   (Lemma).
+//                   Nothing per integer touches HBM.
+//   k_verify        exact rad(n), rad(n+1) of each flagged n by warp-cooperative trial
+//                   division; keeps n with rad(n) rad(n+1) <= 2n  (the "key" test).
+//   k_enumerate     collision pass: every partner m of n lies on the residue class
+//                   m = n - tR (first kind) or m = tR - n - 1 (second kind), R = rad(n)rad(n+1);
+//                   each is checked exactly with gcds (rad(m) == r  <=>  r | m and m/r | r^inf).
+//   k_finalize      exact verification of each match by full radical comparison and the
+//                   reference's classification (signatures.py:67-81).
+// Also: k_sieve_exact (rad(x) materialised, radical.py:109-124), k_trial_division
+// (_kernels.py:87-112) and the prime-table kernels (primes.py:24-35).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bnx_kernels.cuh"
+#include "bnx_math.cuh"
+
+namespace bnx {
+
+// ------------------------------------------------------------------------------------
+// Block-wide exclusive scan of one uint32 per thread (blockDim.x multiple of 32, <= 1024).
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        s_warp[lane] = w;
+    }
+    __syncthreads();
+    uint32_t base = warp ? s_warp[warp - 1] : 0;
+    *total = s_warp[nw - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+// ------------------------------------------------------------------------------------
+// Prime tables (primes.py:24-35).  Base primes <= ls (ls <= 65536) by one block.
+__global__ void k_base_primes(uint32_t ls, uint32_t* out, uint32_t* count) {
+    extern __shared__ uint8_t comp[];
+    __shared__ uint32_t s_warp[32];
+    for (uint32_t i = threadIdx.x; i <= ls; i += blockDim.x) comp[i] = (i < 2);
+    __syncthreads();
+    for (uint32_t d = 2; d * d <= ls; ++d) {
+        if (!comp[d])
+            for (uint32_t k = d * d + threadIdx.x * d; k <= ls; k += blockDim.x * d) comp[k] = 1;
+        __syncthreads();
+    }
+    uint32_t per = (ls + 1 + blockDim.x - 1) / blockDim.x;
+    uint32_t b = threadIdx.x * per, e = min(b + per, ls + 1);
+    uint32_t c = 0;
+    for (uint32_t i = b; i < e; ++i) c += !comp[i];
+    uint32_t total;
+    uint32_t off = block_excl_scan(c, s_warp, &total);
+    for (uint32_t i = b; i < e; ++i)
+        if (!comp[i]) out[off++] = i;
+    if (threadIdx.x == 0) *count = total;
+}
+
+// Segmented Eratosthenes over [lo, hi] in blocks of SEGP numbers, sieving with base
+// primes (ascending, covering isqrt(hi)).  Pass 1 (offsets == nullptr) writes per-block
+// counts; pass 2 writes the primes at the scanned offsets.
+constexpr uint32_t SEGP = 32768;
+__global__ void __launch_bounds__(1024) k_prime_seg(uint64_t lo, uint64_t hi, const uint32_t* base, uint32_t nbase,
+                                                    uint32_t* counts, const uint64_t* offsets, uint32_t* out) {
+    __shared__ uint8_t flag[SEGP];
+    __shared__ uint32_t s_warp[32];
+    const uint64_t s0 = lo + (uint64_t)blockIdx.x * SEGP;
+    const uint32_t len = (uint32_t)min((uint64_t)SEGP, hi - s0 + 1);
+    for (uint32_t i = threadIdx.x; i < SEGP; i += blockDim.x) flag[i] = (i < len) && (s0 + i >= 2);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint64_t last = s0 + len - 1;
+    for (uint32_t j = warp; j < nbase; j += nw) {
+        uint64_t p = base[j];
+        if (p * p > last) break;
+        uint64_t first = p * p;
+        if (first < s0) first = (s0 + p - 1) / p * p;
+        for (uint64_t k = first - s0 + lane * p; k < len; k += 32 * p) flag[k] = 0;
+    }
+    __syncthreads();
+    const uint32_t per = SEGP / blockDim.x;
+    const uint32_t b = threadIdx.x * per;
+    uint32_t c = 0;
+    for (uint32_t i = 0; i < per; ++i) c += flag[b + i];
+    uint32_t total;
+    uint32_t off = block_excl_scan(c, s_warp, &total);
+    if (offsets == nullptr) {
+        if (threadIdx.x == 0) counts[blockIdx.x] = total;
+    } else {
+        uint64_t o = offsets[blockIdx.x] + off;
+        for (uint32_t i = 0; i < per; ++i)
+            if (flag[b + i]) out[o++] = (uint32_t)(s0 + b + i);
+    }
+}
+
+// Exclusive scan of n uint32 counts into uint64 offsets (+ total at offsets[n]); one block.
+__global__ void k_scan_counts(const uint32_t* counts, uint64_t n, uint64_t base, uint64_t* offsets) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = base;
+    __syncthreads();
+    for (uint64_t s = 0; s < n; s += blockDim.x) {
+        uint64_t i = s + threadIdx.x;
+        uint32_t v = i < n ? counts[i] : 0;
+        uint32_t total;
+        uint32_t ex = block_excl_scan(v, s_warp, &total);
+        uint64_t c = carry;
+        if (i < n) offsets[i] = c + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c + total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offsets[n] = carry;
+}
+
+// u64 host primes -> u32 device primes (values < 2^32 by construction).
+__global__ void k_narrow_primes(const uint64_t* in, uint64_t n, uint32_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)in[i];
+}
+__global__ void k_widen_primes(const uint32_t* in, uint64_t n, uint64_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
+// ------------------------------------------------------------------------------------
+// Progression tables: every q = p^e <= max_x, e >= 2 (odd p; p = 2 too when include_two),
+// split at `tile` into the per-tile list (q < tile) and the bucketed list.  Order inside a
+// list is irrelevant: hits commute.  Also the odd-prime exact-division table.
+__device__ uint32_t prime_weight(uint32_t p) {
+    if (p == 2) return 4;
+    return (uint32_t)ceil(4.0 * log2((double)p) + 1e-7);
+}
+
+__global__ void k_build_tables(const uint32_t* primes, uint64_t np, uint64_t max_x, int include_two, uint32_t tile,
+                               BnxProg* small, uint32_t* nsmall, uint32_t small_cap, BnxProg* large,
+                               unsigned long long* nlarge, uint64_t large_cap, BnxPDiv* pdiv, uint64_t* npdiv,
+                               int* overflow) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < np; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = primes[i];
+        if (p * p > max_x) continue;
+        if (p != 2) {
+            // pdiv is indexed like the odd primes, so it stays ascending.
+            uint64_t slot = (primes[0] == 2) ? i - 1 : i;
+            pdiv[slot] = BnxPDiv{p, bnx_inv64(p), ~0ull / p};
+            atomicMax((unsigned long long*)npdiv, (unsigned long long)(slot + 1));
+        }
+        if (p == 2 && !include_two) continue;
+        const uint32_t w = prime_weight((uint32_t)p);
+        uint64_t q = p * p;
+        for (;;) {
+            BnxProg e{q, ~0ull / q, (uint32_t)p, w};
+            if (q < tile) {
+                uint32_t k = atomicAdd(nsmall, 1u);
+                if (k < small_cap) small[k] = e; else *overflow = 1;
+            } else {
+                unsigned long long k = atomicAdd(nlarge, 1ull);
+                if (k < large_cap) large[k] = e; else *overflow = 1;
+            }
+            if (q > max_x / p) break;
+            q *= p;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// THE SCREEN.  One CTA owns a segment of NT tiles of TILE integers; per tile the quarter-bit
+// log-surplus A(x) = sum over p^e | x, e >= 2, of w_p (w_p >= 4 log2 p) is accumulated as
+// packed bytes in shared memory with 32-bit shared atomics:
+//   * q = p^e < TILE:  strided per tile (block-wide for q < 64, warp-wide otherwise);
+//   * q >= TILE:       hits at most once per tile; enumerated once per segment into
+//                      per-tile shared-memory buckets.
+// p = 2 is exact from the bit position (ctz) in the scan.  A pair sum
+//   A(n) + A(n+1) >= 4 log2(s(n) s(n+1))  and  rad(n)rad(n+1) <= 2n  <=>  s(n)s(n+1) >= (n+1)/2,
+// so testing  A(n) + A(n+1) >= floor(4 log2(n+1)) - 5  never drops a candidate.
+template <int TILE, int NT, int THREADS, int BCAP, int MAXS>
+__global__ void __launch_bounds__(THREADS) k_screen(ScreenArgs a) {
+    constexpr int NW = THREADS / 32;
+    constexpr uint32_t SEG = (uint32_t)TILE * NT;
+    constexpr int WORDS = TILE / 4;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* acc = smem;                    // WORDS + 4 (the tile plus 4 integers of the next one)
+    uint32_t* bcnt = acc + WORDS + 4;        // NT
+    uint32_t* bent = bcnt + NT;              // NT * BCAP: (loc | w << 16)
+    uint32_t* s_q = bent + NT * BCAP;        // MAXS
+    uint32_t* s_w = s_q + MAXS;
+    uint32_t* s_tm = s_w + MAXS;
+    uint32_t* s_off = s_tm + MAXS;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nsmall = a.nsmall;
+    for (int j = tid; j < nsmall; j += THREADS) {
+        uint32_t q = (uint32_t)a.small[j].q;
+        s_q[j] = q;
+        s_w[j] = a.small[j].w;
+        s_tm[j] = (uint32_t)TILE % q;
+    }
+
+    for (uint64_t seg = blockIdx.x; seg < a.nseg; seg += gridDim.x) {
+        const uint64_t seg0 = a.x_begin + seg * SEG;
+        __syncthreads();
+        for (int j = tid; j < NT; j += THREADS) bcnt[j] = 0;
+        for (int j = tid; j < nsmall; j += THREADS) {
+            uint64_t o = bnx_first_offset(seg0, s_q[j], a.small[j].recip);
+            if (seg0 == 0 && o == 0) o = s_q[j];  // never sieve x = 0
+            s_off[j] = (uint32_t)o;
+        }
+        __syncthreads();
+        for (int j = tid; j < a.nlarge; j += THREADS) {
+            const BnxProg pr = a.large[j];
+            uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip);
+            if (seg0 == 0 && o == 0) o = pr.q;
+            for (; o < SEG + 4; o += pr.q) {
+                const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
+                const uint32_t ent = pr.w << 16;
+                if (t < NT) {
+                    uint32_t k = atomicAdd(&bcnt[t], 1u);
+                    if (k < BCAP) bent[t * BCAP + k] = loc | ent; else a.flags[0] = 1;
+                }
+                if (loc < 4 && t > 0) {
+                    uint32_t k = atomicAdd(&bcnt[t - 1], 1u);
+                    if (k < BCAP) bent[(t - 1) * BCAP + k] = (loc + TILE) | ent; else a.flags[0] = 1;
+                }
+            }
+        }
+        __syncthreads();
+
+        for (int t = 0; t < NT; ++t) {
+            const uint64_t tile0 = seg0 + (uint64_t)t * TILE;
+            if (tile0 > a.n_last) break;
+            for (int i = tid; i < WORDS + 4; i += THREADS) acc[i] = 0;
+            __syncthreads();
+            // small progressions
+            for (int j = 0; j < nsmall; ++j) {
+                const uint32_t q = s_q[j];
+                if (q >= 64) continue;
+                const uint32_t w = s_w[j];
+                for (uint32_t o = s_off[j] + tid * q; o < TILE + 4; o += THREADS * q)
+                    atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
+            }
+            for (int j = warp; j < nsmall; j += NW) {
+                const uint32_t q = s_q[j];
+                if (q < 64) continue;
+                const uint32_t w = s_w[j];
+                for (uint32_t o = s_off[j] + lane * q; o < TILE + 4; o += 32 * q)
+                    atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
+            }
+            // bucketed large progressions of this tile
+            {
+                const uint32_t nb = min(bcnt[t], (uint32_t)BCAP);
+                for (uint32_t i = tid; i < nb; i += THREADS) {
+                    const uint32_t e = bent[t * BCAP + i];
+                    const uint32_t loc = e & 0xFFFFu;
+                    atomicAdd(&acc[loc >> 2], (e >> 16) << ((loc & 3) << 3));
+                }
+            }
+            __syncthreads();
+            for (int j = tid; j < nsmall; j += THREADS) {
+                int no = (int)s_off[j] - (int)s_tm[j];
+                if (no < 0) no += (int)s_q[j];
+                s_off[j] = (uint32_t)no;
+            }
+            // scan: 4 integers per word, pair sums in 16-bit lanes
+            const bool low = tile0 < 65536;
+            const uint32_t t_tile = low ? 0u : (uint32_t)max(0, bnx_floor4log2(tile0 + 1) - 5);
+            const uint32_t c_first = tile0 ? 4u * (uint32_t)(bnx_ctz64(tile0) - 1) : 0u;
+            const uint64_t next0 = tile0 + TILE;
+            const uint32_t c_next = 4u * (uint32_t)(bnx_ctz64(next0) - 1);
+            for (int j = tid; j < WORDS; j += THREADS) {
+                const uint64_t x0 = tile0 + 4u * (uint32_t)j;
+                const uint32_t tw = low ? (uint32_t)max(0, bnx_floor4log2(x0 + 1) - 5) : t_tile;
+                const uint32_t a0 = acc[j], a1 = acc[j + 1];
+                const uint32_t c0 = j ? 4u * (uint32_t)__ffs(j) : c_first;
+                const uint32_t c4 = (j + 1 < WORDS) ? 4u * (uint32_t)__ffs(j + 1) : c_next;
+                const uint32_t sh = __funnelshift_r(a0, a1, 8);
+                const uint32_t ev = (a0 & 0x00FF00FFu) + (sh & 0x00FF00FFu) + c0;
+                const uint32_t od = ((a0 >> 8) & 0x00FF00FFu) + ((sh >> 8) & 0x00FF00FFu) + (c4 << 16);
+                const uint32_t bias = (0x8000u - tw) * 0x00010001u;
+                const uint32_t he = (ev + bias) & 0x80008000u, ho = (od + bias) & 0x80008000u;
+                if (he | ho) {
+                    uint64_t cand[4];
+                    int nc = 0;
+                    if (he & 0x8000u) cand[nc++] = x0;
+                    if (ho & 0x8000u) cand[nc++] = x0 + 1;
+                    if (he & 0x80000000u) cand[nc++] = x0 + 2;
+                    if (ho & 0x80000000u) cand[nc++] = x0 + 3;
+                    for (int c = 0; c < nc; ++c) {
+                        const uint64_t n = cand[c];
+                        if (n >= a.n_first && n <= a.n_last) {
+                            unsigned long long k = atomicAdd(&a.ctr[0], 1ull);
+                            if (k < a.surv_cap) a.surv[k] = n;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Exact rad(x) by warp-cooperative trial division over the odd-prime table (ascending).
+// Each lane owns primes j = lane (mod 32); the partial products of the primes and of the
+// prime powers dividing x are multiplied across the warp; the cofactor is prime or 1.
+__device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_t npd) {
+    const int lane = threadIdx.x & 31;
+    const int tz = bnx_ctz64(x);
+    const uint64_t y = x >> tz;
+    uint64_t pr = 1, pp = 1;
+    for (uint64_t j = lane; j < npd; j += 32) {
+        const BnxPDiv d = pd[j];
+        if (d.p * d.p > y) break;
+        uint64_t t = y * d.inv;
+        if (t <= d.lim) {
+            pr *= d.p;
+            pp *= d.p;
+            while (t * d.inv <= d.lim) { t *= d.inv; pp *= d.p; }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        pr *= __shfl_xor_sync(0xffffffffu, pr, o);
+        pp *= __shfl_xor_sync(0xffffffffu, pp, o);
+    }
+    const uint64_t cof = y * bnx_inv64(pp);
+    return (tz ? 2ull : 1ull) * pr * (cof > 1 ? cof : 1ull);
+}
+
+__global__ void k_verify(VerifyArgs a) {
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint64_t cnt = min((uint64_t)a.ctr[0], a.surv_cap);
+    for (uint64_t i = gw; i < cnt; i += nwarps) {
+        const uint64_t n = a.surv[i];
+        const uint64_t r0 = rad_warp(n, a.pdiv, a.npdiv);
+        const uint64_t r1 = rad_warp(n + 1, a.pdiv, a.npdiv);
+        if ((threadIdx.x & 31) == 0 && __umul64hi(r0, r1) == 0 && r0 * r1 <= 2 * n) {
+            unsigned long long k = atomicAdd(&a.ctr[1], 1ull);
+            if (k < a.cand_cap) a.cand[k] = BnxCand{n, r0, r1};
+        }
+    }
+}
+
+// Collision pass on the residue classes.  For a pair m < n with S_m = S_n:
+//   first kind  rad(n) | n-m and rad(n+1) | n-m  ->  R | n - m      (m = n - tR,  t >= 1)
+//   second kind rad(n) | n+m+1 and rad(n+1) | n+m+1 -> R | n + m + 1 (m = tR - n - 1)
+// Each m is accepted iff rad(m), rad(m+1) equal the required radicals, tested exactly:
+// rad(m) == r  <=>  r | m  and  m / r | r^inf.
+__global__ void k_enumerate(EnumArgs a) {
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const uint64_t cnt = min((uint64_t)a.ctr[1], a.cand_cap);
+    for (uint64_t i = gw; i < cnt; i += nwarps) {
+        const BnxCand c = a.cand[i];
+        const uint64_t n = c.n, R = c.r0 * c.r1;
+        const uint64_t t1 = (a.kinds & 1u) ? (n - 1) / R : 0;                // m = n - tR >= 1
+        const uint64_t t0 = (n + 1) / R + 1, t2 = (2 * n) / R;                 // n+2 <= tR <= 2n
+        const uint64_t c2 = ((a.kinds & 2u) && t2 >= t0) ? t2 - t0 + 1 : 0;
+        const uint64_t total = t1 + c2;
+        if (lane == 0 && total) atomicAdd(&a.ctr[2], (unsigned long long)total);
+        for (uint64_t k = lane; k < total; k += 32) {
+            uint64_t m, ra, rb;
+            uint32_t kind;
+            if (k < t1) { m = n - (k + 1) * R; ra = c.r0; rb = c.r1; kind = 1; }
+            else { m = (t0 + (k - t1)) * R - n - 1; ra = c.r1; rb = c.r0; kind = 2; }
+            // rad(m) == ra and rad(m+1) == rb
+            if (m % ra == 0 && (m + 1) % rb == 0 && bnx_supported_by(m / ra, ra) && bnx_supported_by((m + 1) / rb, rb)) {
+                unsigned long long s = atomicAdd(&a.ctr[3], 1ull);
+                if (s < a.match_cap) a.match[s] = BnxMatch{m, n, kind, 0};
+            }
+        }
+    }
+}
+
+// Exact verification by full radical comparison + classification (signatures.py:67-81).
+__global__ void k_finalize(FinalArgs a) {
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint64_t cnt = min((uint64_t)a.ctr[3], a.match_cap);
+    for (uint64_t i = gw; i < cnt; i += nwarps) {
+        const BnxMatch mt = a.match[i];
+        const uint64_t rm = rad_warp(mt.m, a.pdiv, a.npdiv), rm1 = rad_warp(mt.m + 1, a.pdiv, a.npdiv);
+        const uint64_t rn = rad_warp(mt.n, a.pdiv, a.npdiv), rn1 = rad_warp(mt.n + 1, a.pdiv, a.npdiv);
+        int kind = 0;
+        if (rm == rn && rm1 == rn1) kind = 1;
+        else if (rm == rn1 && rm1 == rn) kind = 2;
+        if ((threadIdx.x & 31) == 0 && kind && (a.kinds & (1u << (kind - 1))) && mt.m >= 1 && mt.m < mt.n) {
+            unsigned long long s = atomicAdd(&a.ctr[4], 1ull);
+            if (s < a.pair_cap) a.pairs[s] = bnx_pair_t{mt.m, mt.n, rm, rm1, kind, 0};
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// rad(x) materialised (radical.py:109-124 / _kernels.py:48-84): u64 tiles in shared memory,
+// start value x (or x with surplus twos stripped, _kernels.py:33-45), each hit of p^e
+// divides the slot by p exactly (multiply by p^-1 mod 2^64; shift for p = 2) through a
+// 64-bit shared CAS so concurrent progressions on one slot compose.
+__device__ __forceinline__ void div_slot(unsigned long long* s, uint64_t inv, bool two) {
+    unsigned long long old = *s, assumed;
+    do {
+        assumed = old;
+        const unsigned long long nv = two ? (assumed >> 1) : assumed * inv;
+        old = atomicCAS(s, assumed, nv);
+    } while (old != assumed);
+}
+
+template <int TILE, int NT, int THREADS, int BCAP, int MAXS>
+__global__ void __launch_bounds__(THREADS) k_sieve_exact(SieveArgs a) {
+    constexpr int NW = THREADS / 32;
+    constexpr uint64_t SEG = (uint64_t)TILE * NT;
+    extern __shared__ __align__(16) unsigned long long sm64[];
+    unsigned long long* r = sm64;                        // TILE
+    unsigned long long* bent = r + TILE;                 // NT * BCAP : (prog index << 16 | loc)
+    unsigned long long* s_inv = bent + NT * BCAP;        // MAXS
+    uint32_t* bcnt = (uint32_t*)(s_inv + MAXS);          // NT
+    uint32_t* s_q = bcnt + NT;                           // MAXS
+    uint32_t* s_tm = s_q + MAXS;
+    uint32_t* s_off = s_tm + MAXS;
+    uint32_t* s_two = s_off + MAXS;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nsmall = a.nsmall;
+    for (int j = tid; j < nsmall; j += THREADS) {
+        const uint32_t q = (uint32_t)a.small[j].q, p = a.small[j].p;
+        s_q[j] = q;
+        s_tm[j] = (uint32_t)TILE % q;
+        s_two[j] = (p == 2);
+        s_inv[j] = (p == 2) ? 0ull : bnx_inv64(p);
+    }
+    const uint64_t nseg = (a.length + SEG - 1) / SEG;
+    for (uint64_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+        const uint64_t seg_off = seg * SEG;
+        const uint64_t seg0 = a.start + seg_off;
+        __syncthreads();
+        for (int j = tid; j < NT; j += THREADS) bcnt[j] = 0;
+        for (int j = tid; j < nsmall; j += THREADS) s_off[j] = (uint32_t)bnx_first_offset(seg0, s_q[j], a.small[j].recip);
+        __syncthreads();
+        for (uint64_t j = tid; j < a.nlarge; j += THREADS) {
+            const BnxProg pr = a.large[j];
+            uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip);
+            while (o < SEG) {
+                const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
+                uint32_t k = atomicAdd(&bcnt[t], 1u);
+                if (k < BCAP) bent[t * BCAP + k] = (j << 16) | loc; else a.flags[0] = 1;
+                if (pr.q >= SEG) break;
+                o += pr.q;
+            }
+        }
+        __syncthreads();
+        for (int t = 0; t < NT; ++t) {
+            const uint64_t toff = seg_off + (uint64_t)t * TILE;
+            if (toff >= a.length) break;
+            const uint64_t tile0 = a.start + toff;
+            for (int i = tid; i < TILE; i += THREADS) {
+                const uint64_t x = tile0 + (uint64_t)i;
+                uint64_t v = x;
+                if (a.fast && x) {
+                    const int tz = bnx_ctz64(x);
+                    if (tz >= 2) v = x >> (tz - 1);
+                }
+                r[i] = v;
+            }
+            __syncthreads();
+            for (int j = 0; j < nsmall; ++j) {
+                const uint32_t q = s_q[j];
+                if (q >= 64) continue;
+                const uint64_t inv = s_inv[j];
+                const bool two = s_two[j];
+                for (uint32_t o = s_off[j] + tid * q; o < TILE; o += THREADS * q) div_slot(&r[o], inv, two);
+            }
+            for (int j = warp; j < nsmall; j += NW) {
+                const uint32_t q = s_q[j];
+                if (q < 64) continue;
+                const uint64_t inv = s_inv[j];
+                const bool two = s_two[j];
+                for (uint32_t o = s_off[j] + lane * q; o < TILE; o += 32 * q) div_slot(&r[o], inv, two);
+            }
+            {
+                const uint32_t nb = min(bcnt[t], (uint32_t)BCAP);
+                for (uint32_t i = tid; i < nb; i += THREADS) {
+                    const unsigned long long e = bent[t * BCAP + i];
+                    const uint32_t p = a.large[e >> 16].p;
+                    div_slot(&r[e & 0xFFFFu], p == 2 ? 0ull : bnx_inv64(p), p == 2);
+                }
+            }
+            __syncthreads();
+            for (int j = tid; j < nsmall; j += THREADS) {
+                int no = (int)s_off[j] - (int)s_tm[j];
+                if (no < 0) no += (int)s_q[j];
+                s_off[j] = (uint32_t)no;
+            }
+            const uint64_t rem = a.length - toff;
+            const int lim = rem < (uint64_t)TILE ? (int)rem : TILE;
+            uint64_t* dst = a.out + toff;
+            if (lim == TILE && ((((uintptr_t)dst) & 15) == 0)) {
+                for (int i = tid; i < TILE / 2; i += THREADS)
+                    reinterpret_cast<ulonglong2*>(dst)[i] = make_ulonglong2(r[2 * i], r[2 * i + 1]);
+            } else {
+                for (int i = tid; i < lim; i += THREADS) dst[i] = r[i];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// _kernels.py:87-112 on the GPU: one thread per integer, trial division by the odd primes.
+__global__ void k_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < length; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = start + k;
+        const int tz = bnx_ctz64(x);
+        uint64_t y = x >> tz;
+        uint64_t r = tz ? 2 : 1;
+        for (uint64_t j = 0; j < npd; ++j) {
+            const BnxPDiv d = pd[j];
+            if (d.p * d.p > y) break;
+            uint64_t t = y * d.inv;
+            if (t <= d.lim) {
+                r *= d.p;
+                do { y = t; t = y * d.inv; } while (t <= d.lim);
+            }
+        }
+        if (y > 1) r *= y;
+        out[k] = r;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Launch helpers (instantiations and dynamic shared memory sizes).
+size_t screen_smem_bytes() {
+    return sizeof(uint32_t) * ((size_t)(SCREEN_TILE / 4 + 4) + SCREEN_NT + (size_t)SCREEN_NT * SCREEN_BCAP + 4 * SCREEN_MAXS);
+}
+size_t sieve_smem_bytes() {
+    return sizeof(unsigned long long) * ((size_t)SIEVE_TILE + (size_t)SIEVE_NT * SIEVE_BCAP + SIEVE_MAXS) +
+           sizeof(uint32_t) * ((size_t)SIEVE_NT + 4 * SIEVE_MAXS);
+}
+
+const void* screen_kernel() {
+    return (const void*)k_screen<SCREEN_TILE, SCREEN_NT, SCREEN_THREADS, SCREEN_BCAP, SCREEN_MAXS>;
+}
+const void* sieve_kernel() {
+    return (const void*)k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>;
+}
+
+void launch_screen(const ScreenArgs& a, int grid, cudaStream_t st) {
+    k_screen<SCREEN_TILE, SCREEN_NT, SCREEN_THREADS, SCREEN_BCAP, SCREEN_MAXS>
+        <<<grid, SCREEN_THREADS, screen_smem_bytes(), st>>>(a);
+}
+void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st) {
+    k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>
+        <<<grid, SIEVE_THREADS, sieve_smem_bytes(), st>>>(a);
+}
+void launch_verify(const VerifyArgs& a, int grid, cudaStream_t st) { k_verify<<<grid, 256, 0, st>>>(a); }
+void launch_enumerate(const EnumArgs& a, int grid, cudaStream_t st) { k_enumerate<<<grid, 256, 0, st>>>(a); }
+void launch_finalize(const FinalArgs& a, int grid, cudaStream_t st) { k_finalize<<<grid, 256, 0, st>>>(a); }
+
+void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st) {
+    if (ls + 1 > 48 * 1024) cudaFuncSetAttribute(k_base_primes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ls + 1));
+    k_base_primes<<<1, 1024, ls + 1, st>>>(ls, out, count);
+}
+void launch_prime_seg(uint64_t lo, uint64_t hi, const uint32_t* base, uint32_t nbase, uint32_t* counts,
+                      const uint64_t* offsets, uint32_t* out, uint64_t nblocks, cudaStream_t st) {
+    k_prime_seg<<<(unsigned)nblocks, 1024, 0, st>>>(lo, hi, base, nbase, counts, offsets, out);
+}
+void launch_scan_counts(const uint32_t* counts, uint64_t n, uint64_t base, uint64_t* offsets, cudaStream_t st) {
+    k_scan_counts<<<1, 1024, 0, st>>>(counts, n, base, offsets);
+}
+void launch_narrow(const uint64_t* in, uint64_t n, uint32_t* out, cudaStream_t st) {
+    k_narrow_primes<<<256, 256, 0, st>>>(in, n, out);
+}
+void launch_widen(const uint32_t* in, uint64_t n, uint64_t* out, cudaStream_t st) {
+    k_widen_primes<<<256, 256, 0, st>>>(in, n, out);
+}
+void launch_build_tables(const uint32_t* primes, uint64_t np, uint64_t max_x, int include_two, uint32_t tile,
+                         BnxProg* small, uint32_t* nsmall, uint32_t small_cap, BnxProg* large,
+                         unsigned long long* nlarge, uint64_t large_cap, BnxPDiv* pdiv, uint64_t* npdiv,
+                         int* overflow, cudaStream_t st) {
+    k_build_tables<<<256, 256, 0, st>>>(primes, np, max_x, include_two, tile, small, nsmall, small_cap, large, nlarge,
+                                        large_cap, pdiv, npdiv, overflow);
+}
+void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out,
+                           int grid, cudaStream_t st) {
+    k_trial_division<<<grid, 256, 0, st>>>(start, length, pd, npd, out);
+}
+
+}  // namespace bnx

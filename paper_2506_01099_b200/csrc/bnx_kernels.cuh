@@ -1,0 +1,107 @@
+// bnx_kernels.cuh -- kernel argument blocks, tile geometry and launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/benelux_b200.h"
+#include "bnx_math.cuh"
+
+namespace bnx {
+
+// Screen geometry: a tile is 32768 integers (one byte each, 32 KB of shared memory), a
+// segment is SCREEN_NT tiles; progressions q >= SCREEN_TILE hit a tile at most once and go
+// through per-tile buckets of SCREEN_BCAP entries (expected ~40 per tile).
+constexpr int SCREEN_TILE = 32768;
+constexpr int SCREEN_NT = 32;
+constexpr int SCREEN_THREADS = 512;
+constexpr int SCREEN_BCAP = 128;
+constexpr int SCREEN_MAXS = 160;
+
+// Exact radical sieve geometry: 4096 u64 slots per tile (32 KB).
+constexpr int SIEVE_TILE = 4096;
+constexpr int SIEVE_NT = 64;
+constexpr int SIEVE_THREADS = 256;
+constexpr int SIEVE_BCAP = 64;
+constexpr int SIEVE_MAXS = 160;
+
+// Counter block (device): [0] survivors [1] candidates [2] residue checks [3] matches [4] pairs
+constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_N = 8;
+
+struct ScreenArgs {
+    uint64_t x_begin;  // multiple of SCREEN_TILE
+    uint64_t nseg;
+    uint64_t n_first, n_last;
+    const BnxProg* small;
+    int nsmall;
+    const BnxProg* large;
+    int nlarge;
+    uint64_t* surv;
+    uint64_t surv_cap;
+    unsigned long long* ctr;
+    int* flags;  // [0] bucket overflow
+};
+
+struct VerifyArgs {
+    const uint64_t* surv;
+    uint64_t surv_cap;
+    const BnxPDiv* pdiv;
+    uint64_t npdiv;
+    BnxCand* cand;
+    uint64_t cand_cap;
+    unsigned long long* ctr;
+};
+
+struct EnumArgs {
+    const BnxCand* cand;
+    uint64_t cand_cap;
+    uint32_t kinds;
+    BnxMatch* match;
+    uint64_t match_cap;
+    unsigned long long* ctr;
+};
+
+struct FinalArgs {
+    const BnxMatch* match;
+    uint64_t match_cap;
+    const BnxPDiv* pdiv;
+    uint64_t npdiv;
+    uint32_t kinds;
+    bnx_pair_t* pairs;
+    uint64_t pair_cap;
+    unsigned long long* ctr;
+};
+
+struct SieveArgs {
+    uint64_t start, length;
+    const BnxProg* small;
+    int nsmall;
+    const BnxProg* large;
+    uint64_t nlarge;
+    int fast;
+    uint64_t* out;
+    int* flags;
+};
+
+size_t screen_smem_bytes();
+size_t sieve_smem_bytes();
+const void* screen_kernel();
+const void* sieve_kernel();
+void launch_screen(const ScreenArgs& a, int grid, cudaStream_t st);
+void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st);
+void launch_verify(const VerifyArgs& a, int grid, cudaStream_t st);
+void launch_enumerate(const EnumArgs& a, int grid, cudaStream_t st);
+void launch_finalize(const FinalArgs& a, int grid, cudaStream_t st);
+void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st);
+void launch_prime_seg(uint64_t lo, uint64_t hi, const uint32_t* base, uint32_t nbase, uint32_t* counts,
+                      const uint64_t* offsets, uint32_t* out, uint64_t nblocks, cudaStream_t st);
+void launch_scan_counts(const uint32_t* counts, uint64_t n, uint64_t base, uint64_t* offsets, cudaStream_t st);
+void launch_narrow(const uint64_t* in, uint64_t n, uint32_t* out, cudaStream_t st);
+void launch_widen(const uint32_t* in, uint64_t n, uint64_t* out, cudaStream_t st);
+void launch_build_tables(const uint32_t* primes, uint64_t np, uint64_t max_x, int include_two, uint32_t tile,
+                         BnxProg* small, uint32_t* nsmall, uint32_t small_cap, BnxProg* large,
+                         unsigned long long* nlarge, uint64_t large_cap, BnxPDiv* pdiv, uint64_t* npdiv,
+                         int* overflow, cudaStream_t st);
+void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out,
+                           int grid, cudaStream_t st);
+
+}  // namespace bnx

@@ -1,0 +1,91 @@
+// bnx_math.cuh -- 64-bit integer helpers shared by the Benelux-pair kernels (sm_100a).
+//
+// No hardware u64 divide exists on the GPU, so the hot loops never divide:
+//  * exact division by an odd prime p is a multiply by p^-1 mod 2^64 (Newton inverse);
+//  * "p | x" for odd p is  x * p^-1 (mod 2^64) <= floor((2^64-1)/p);
+//  * a residue a mod q uses a precomputed reciprocal floor((2^64-1)/q) and __umul64hi.
+#pragma once
+#include <stdint.h>
+
+#define BNX_HD __host__ __device__ __forceinline__
+#define BNX_D __device__ __forceinline__
+
+// Inverse of odd a modulo 2^64 (Newton: 3 -> 6 -> 12 -> 24 -> 48 -> 96 correct bits).
+BNX_HD uint64_t bnx_inv64(uint64_t a) {
+    uint64_t x = a;
+    for (int i = 0; i < 5; ++i) x *= 2 - a * x;
+    return x;
+}
+
+BNX_D int bnx_ctz64(uint64_t x) { return __ffsll((long long)x) - 1; }
+
+// a mod q given recip = floor((2^64-1)/q); at most two corrections.
+BNX_D uint64_t bnx_mod(uint64_t a, uint64_t q, uint64_t recip) {
+    uint64_t t = __umul64hi(a, recip);
+    uint64_t r = a - t * q;
+    while (r >= q) r -= q;
+    return r;
+}
+
+// Smallest o >= 0 with (base + o) % q == 0.
+BNX_D uint64_t bnx_first_offset(uint64_t base, uint64_t q, uint64_t recip) {
+    uint64_t r = bnx_mod(base, q, recip);
+    return r ? q - r : 0;
+}
+
+BNX_D uint64_t bnx_gcd64(uint64_t a, uint64_t b) {
+    if (a == 0) return b;
+    if (b == 0) return a;
+    int sh = bnx_ctz64(a | b);
+    a >>= bnx_ctz64(a);
+    do {
+        b >>= bnx_ctz64(b);
+        if (a > b) { uint64_t t = a; a = b; b = t; }
+        b -= a;
+    } while (b);
+    return a << sh;
+}
+
+// u | r^inf, i.e. every prime of u divides r (rad(u) | r).  u >= 1, r >= 1.
+BNX_D bool bnx_supported_by(uint64_t u, uint64_t r) {
+    while (u > 1) {
+        uint64_t g = bnx_gcd64(u, r);
+        if (g == 1) return false;
+        u /= g;
+    }
+    return true;
+}
+
+// floor(4 * log2(v)) for v >= 1, exact: 4e + #{k in 1..3 : mantissa >= 2^(k/4)}.
+// The constants are ceil(2^(63 + k/4)), computed with integer roots.
+BNX_D int bnx_floor4log2(uint64_t v) {
+    int lz = __clzll((long long)v);
+    uint64_t m = v << lz;
+    int e = 63 - lz;
+    return 4 * e + (m >= 0x9837f0518db8a970ull) + (m >= 0xb504f333f9de6485ull) + (m >= 0xd744fccad69d6af5ull);
+}
+
+// A prime power progression q = p^e (e >= 2) of the sieve, with its reciprocal and the
+// screen weight w = ceil(4 log2 p) (quarter-bits of log2 p, rounded up).
+struct BnxProg {
+    uint64_t q;
+    uint64_t recip;
+    uint32_t p;
+    uint32_t w;
+};
+
+// An odd prime with its exact-division constants (trial division / verification).
+struct BnxPDiv {
+    uint64_t p;
+    uint64_t inv;
+    uint64_t lim;  // floor((2^64-1)/p)
+};
+
+// Candidate n with rad(n) * rad(n+1) <= 2n, and a signature match (m, n).
+struct BnxCand {
+    uint64_t n, r0, r1;
+};
+struct BnxMatch {
+    uint64_t m, n;
+    uint32_t kind, pad;
+};

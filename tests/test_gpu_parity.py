@@ -1,0 +1,171 @@
+"""GPU parity: the sm_100a path against the reference's golden outputs and the C oracle.
+
+Every test calls through the C ABI (libbenelux_b200.so via paper_2506_01099_b200._native).
+Integer work, so the bar is bit-exact everywhere.
+"""
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from conftest import pair_keys, rows_of
+
+pytestmark = pytest.mark.gpu
+
+bp = pytest.importorskip("paper_2506_01099_b200")
+
+
+def digest(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<u8").tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------- primes (a1) -------------
+def test_primes_match_reference(golden):
+    for lim, rec in golden["primes"].items():
+        pl = bp.primes_up_to(int(lim))
+        assert len(pl) == rec["count"], lim
+        assert digest(pl.primes) == rec["sha256"], lim
+        assert pl.limit == int(lim)
+
+
+# ---------------------------------------------------------------- sieve (a2-a6) -----------
+def test_sieve_small_vectors(golden):
+    p2k = bp.primes_up_to(2000)
+    assert bp.sieve_radicals(bp.Interval(1, 10), p2k).values.tolist() == golden["sieve_small"]["1_10"]
+    assert bp.sieve_radicals(bp.Interval(16, 1), p2k).values.tolist() == golden["sieve_small"]["16_1"]
+    seg = bp.sieve_radicals(bp.Interval.closed(1213, 1218), p2k)
+    assert seg.values.tolist() == golden["sieve_small"]["1213_6"] == [1213, 1214, 15, 38, 1217, 1218]
+
+
+@pytest.mark.parametrize("idx", range(12))
+def test_sieve_windows(golden, idx):
+    w = golden["sieve_windows"][idx]
+    iv = bp.Interval(w["start"], w["length"])
+    primes = bp.primes_up_to(bp.required_prime_bound(iv))
+    vals = bp.sieve_radicals(iv, primes, ctz_fast_path=w["fast"]).values
+    assert vals[:8].tolist() == w["head"]
+    assert vals[-8:].tolist() == w["tail"]
+    assert digest(vals) == w["sha256"]
+
+
+def test_sieve_rejects_uncovered():
+    with pytest.raises(ValueError):
+        bp.sieve_radicals(bp.Interval(1, 1000), bp.primes_up_to(10))
+
+
+def test_sieve_random_windows_vs_oracle(orc):
+    rng = np.random.default_rng(20260811)
+    for _ in range(40):
+        start = int(rng.integers(1, 10**12))
+        length = int(rng.integers(1, 300_000))
+        fast = bool(rng.integers(0, 2))
+        iv = bp.Interval(start, length)
+        need = bp.required_prime_bound(iv)
+        got = bp.sieve_radicals(iv, bp.primes_up_to(need), ctz_fast_path=fast).values
+        want = orc.sieve_segment(start, length, orc.primes_up_to(need), fast)
+        assert np.array_equal(got, want), (start, length, fast)
+
+
+def test_sieve_large_window_vs_trial_division(orc):
+    # a window spanning several segments and grid waves
+    iv = bp.Interval(2**32 - 5_000_000, 12_000_000)
+    got = bp.sieve_radicals(iv).values
+    want = orc.sieve_segment(iv.start, iv.length, orc.primes_up_to(bp.required_prime_bound(iv)))
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- trial division ---------
+def test_trial_division_vectors(golden):
+    for rec in golden["trial_division"]:
+        v = bp.radicals_by_trial_division(bp.Interval(rec["start"], rec["length"]))
+        assert v[:8].tolist() == rec["head"]
+        assert digest(v) == rec["sha256"]
+
+
+# ---------------------------------------------------------------- search (a7-a16) --------
+@pytest.mark.parametrize("limit", ["3", "4", "10", "50", "517", "1300", "2000", "5000", "20000", "30000",
+                                   "1000000", "1048576", "10000000", "16777216"])
+def test_find_pairs_sorted_golden(golden, limit):
+    got = rows_of(bp.find_pairs_sorted(int(limit)))
+    assert got == golden["find_pairs_sorted"][limit]
+
+
+def test_find_pairs_matches_brute_force_golden(golden):
+    for lim, rows in golden["brute_force"].items():
+        assert pair_keys(bp.find_pairs_sorted(int(lim))) == pair_keys(rows)
+
+
+def test_all_limits_up_to_600_vs_oracle_brute_force(orc):
+    for limit in range(3, 600):
+        got = [tuple(r) for r in rows_of(bp.find_pairs_sorted(limit))]
+        assert got == orc.brute_force(limit), limit
+
+
+def test_random_limits_vs_oracle(orc):
+    rng = np.random.default_rng(7)
+    for limit in rng.integers(3, 3_000_000, 12).tolist():
+        got = [tuple(r) for r in rows_of(bp.find_pairs_sorted(int(limit)))]
+        assert got == orc.find_pairs_sorted(int(limit)), limit
+
+
+@pytest.mark.parametrize("case", ["1048576_4096", "1048576_65536", "20000_64", "5000_300", "10000000_131072"])
+def test_run_full_chunked_golden(golden, case):
+    limit, chunk = (int(x) for x in case.split("_"))
+    assert rows_of(bp.run_full_chunked(limit, chunk)) == golden["run_full_chunked"][case]
+
+
+def test_run_full_chunked_resume_golden(golden):
+    got = rows_of(bp.run_full_chunked(5000, 300, resume_from=8))
+    assert got == golden["run_full_chunked"]["5000_300_resume8"]
+
+
+def test_search_chunk_golden(golden):
+    g = golden["search_chunk"]
+    assert rows_of(bp.search_chunk(0, 1300, bp.primes_up_to(2000))) == g["0_1300_p2000"]
+    assert rows_of(bp.search_chunk(0, 10001, bp.primes_up_to(101))) == g["0_10001_p101"]
+    p = bp.primes_up_to(math.isqrt(bp.chunk_bounds(1, 1000).last))
+    assert rows_of(bp.search_chunk(1, 1000, p)) == g["1_1000"]
+    assert rows_of(bp.search_chunk(3, 100, bp.primes_up_to(2000))) == g["3_100_p2000"] == []
+    assert rows_of(bp.search_chunk(1, 40000, bp.primes_up_to(300))) == g["1_40000_p300"]
+
+
+def test_chunk_callback_order():
+    events = []
+    gen = bp.run_full_chunked(80_000, 1 << 12, on_chunk_done=lambda i: events.append(("done", i)))
+    for pair in gen:
+        events.append(("pair", pair.n))
+    done = [e for e in events if e[0] == "done"]
+    assert done == [("done", i) for i in range(bp.num_chunks(80_000, 1 << 12))]
+    for pos, ev in enumerate(events):
+        if ev[0] == "pair":
+            boundary = next(i for kind, i in events[pos:] if kind == "done")
+            assert ev[1] <= bp.chunk_bounds(boundary, 1 << 12).domain_last
+
+
+@pytest.mark.parametrize("limit", ["1048576", "16777216", "10000000", "268435456", "4294967296"])
+def test_known_solutions(golden, limit):
+    exp = golden["expected_pairs_up_to"][limit]
+    got = bp.find_pairs_sorted(int(limit))
+    assert rows_of([p for p in got if p.kind == bp.Kind.FIRST]) == sorted(exp["first"], key=lambda r: (r[1], r[2]))
+    assert rows_of([p for p in got if p.kind == bp.Kind.SECOND]) == sorted(exp["second"], key=lambda r: (r[1], r[2]))
+
+
+def test_kind_filters_2p32(golden):
+    exp = golden["expected_pairs_up_to"]["4294967296"]
+    first = bp.find_pairs(2**32, kinds=bp.Kind.FIRST)
+    second = bp.find_pairs(2**32, kinds=bp.Kind.SECOND)
+    assert rows_of(first) == sorted(exp["first"], key=lambda r: (r[1], r[2]))
+    assert rows_of(second) == sorted(exp["second"], key=lambda r: (r[1], r[2]))
+    assert len(first) == 16 and len(second) == 17
+
+
+def test_errors():
+    with pytest.raises(ValueError):
+        bp.find_pairs_sorted(2)
+    with pytest.raises(bp.MemoryBudgetExceeded, match="chunked"):
+        bp.find_pairs_sorted(10**6, memory_budget_bytes=10**6)
+    with pytest.raises(ValueError):
+        list(bp.run_full_chunked(2, 300))
+    with pytest.raises(ValueError):
+        list(bp.run_full_chunked(5000, 2))
