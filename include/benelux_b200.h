@@ -94,6 +94,11 @@ BNX_API int bnx_ctx_create(int device, bnx_ctx_t** out);
 BNX_API int bnx_ctx_destroy(bnx_ctx_t* ctx);
 BNX_API int bnx_ctx_set_stream(bnx_ctx_t* ctx, void* stream);
 BNX_API int bnx_ctx_stats(const bnx_ctx_t* ctx, bnx_stats_t* out);
+/* Kernel timing with CUDA events on the context stream: when enabled, each search records
+ * events around the screen kernel and around the whole device pipeline; bnx_ctx_timing
+ * returns the last search's milliseconds (valid after bnx_search_collect / bnx_search*). */
+BNX_API int bnx_ctx_set_timing(bnx_ctx_t* ctx, int enabled);
+BNX_API int bnx_ctx_timing(const bnx_ctx_t* ctx, float* screen_ms, float* pipeline_ms);
 
 /* primes.py:24-35: all primes <= limit, ascending.  *count always receives the total;
  * BNX_BUFFER_FULL if it exceeds cap. */

@@ -312,6 +312,7 @@ typedef struct {
     const uint64_t* slots;
     uint64_t mask;
     uint64_t j_begin, j_end, j_step; /* earlier chunks this worker probes */
+    uint64_t sub_len;                /* >0: probe only the first sub_len values of each */
     orc_pairs_t out;
     int status;
 } probe_job_t;
@@ -321,10 +322,11 @@ static void* probe_worker(void* arg) {
     uint64_t s = job->chunk_size;
     uint64_t* vals = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)s);
     if (!vals) { job->status = ORC_STATUS_NOMEM; return NULL; }
+    uint64_t len = job->sub_len ? job->sub_len + 1 : s;
     for (uint64_t j = job->j_begin; j < job->j_end; j += job->j_step) {
         uint64_t first = 1 + j * (s - 1);
-        orc_sieve_segment(first, (size_t)s, job->primes, job->nprimes, 1, vals);
-        int st = orc_probe_table(first, vals, vals + 1, (size_t)(s - 1), job->domain_start, job->cur_vals,
+        orc_sieve_segment(first, (size_t)len, job->primes, job->nprimes, 1, vals);
+        int st = orc_probe_table(first, vals, vals + 1, (size_t)(len - 1), job->domain_start, job->cur_vals,
                                  job->cur_vals + 1, job->slots, job->mask, HASH_PHI, HASH_MUL1, HASH_MUL2,
                                  &job->out);
         if (st != ORC_STATUS_OK && job->status == ORC_STATUS_OK) job->status = st;
@@ -333,15 +335,11 @@ static void* probe_worker(void* arg) {
     return NULL;
 }
 
-/*
- * chunked.py:307-359 -- all pairs whose n lies in chunk `index`'s domain, probing the
- * earlier chunks j in [j_lo, j_hi) only (the full search uses j_lo=0, j_hi=index; the
- * bench samples a subrange).  `slots` (table_size u64) and `vals` (chunk_size u64)
- * are caller scratch.  Timings of the build and probe phases are returned.
- */
-int orc_search_chunk(uint64_t index, uint64_t chunk_size, const uint64_t* primes, size_t nprimes,
-                     uint64_t n_limit, int threads, uint64_t j_lo, uint64_t j_hi, uint64_t* slots,
-                     uint64_t table_size, uint64_t* vals, orc_pairs_t* out, double* t_build, double* t_probe) {
+/* chunked.py:326-333 -- sieve chunk `index` into vals and build its table (intra-chunk
+ * pairs appended to out).  Returns the build status; *t_build gets the wall seconds. */
+int orc_build_chunk(uint64_t index, uint64_t chunk_size, const uint64_t* primes, size_t nprimes,
+                    uint64_t n_limit, uint64_t* slots, uint64_t table_size, uint64_t* vals, orc_pairs_t* out,
+                    double* t_build) {
     uint64_t s = chunk_size;
     uint64_t first = 1 + index * (s - 1);
     double t0 = now_s();
@@ -350,9 +348,19 @@ int orc_search_chunk(uint64_t index, uint64_t chunk_size, const uint64_t* primes
     size_t inserted = 0;
     int status = orc_build_table(first, vals, vals + 1, (size_t)(s - 1), n_limit, slots, table_size - 1,
                                  HASH_PHI, HASH_MUL1, HASH_MUL2, out, &inserted);
-    if (status == ORC_STATUS_TABLE_FULL) return status;
+    if (t_build) *t_build = now_s() - t0;
+    return status;
+}
+
+/* chunked.py:335-356 -- re-sieve the earlier chunks j in [j_lo, j_hi) and probe the table of
+ * chunk `index` (built by orc_build_chunk) with them, on `threads` pthreads. */
+int orc_probe_chunks(uint64_t index, uint64_t chunk_size, const uint64_t* primes, size_t nprimes, int threads,
+                     uint64_t j_lo, uint64_t j_hi, const uint64_t* slots, uint64_t table_size,
+                     const uint64_t* vals, uint64_t sub_len, orc_pairs_t* out, double* t_probe) {
+    uint64_t s = chunk_size;
+    uint64_t first = 1 + index * (s - 1);
     double t1 = now_s();
-    if (t_build) *t_build = t1 - t0;
+    int status = ORC_STATUS_OK;
     if (j_hi > j_lo) {
         if (threads < 1) threads = 1;
         uint64_t njobs = j_hi - j_lo;
@@ -365,6 +373,7 @@ int orc_search_chunk(uint64_t index, uint64_t chunk_size, const uint64_t* primes
             jb->chunk_size = s; jb->primes = primes; jb->nprimes = nprimes;
             jb->domain_start = first; jb->cur_vals = vals; jb->slots = slots; jb->mask = table_size - 1;
             jb->j_begin = j_lo + (uint64_t)w; jb->j_end = j_hi; jb->j_step = (uint64_t)threads;
+            jb->sub_len = sub_len < s - 1 ? sub_len : 0;
             jb->out.cap = per_cap;
             jb->out.kind = (int8_t*)malloc(per_cap + 1);
             jb->out.m = (uint64_t*)malloc(8 * (per_cap + 1));
@@ -381,6 +390,7 @@ int orc_search_chunk(uint64_t index, uint64_t chunk_size, const uint64_t* primes
             for (size_t t = 0; t < k; ++t)
                 if (push_pair(out, jb->out.kind[t], jb->out.m[t], jb->out.n[t], jb->out.rm[t], jb->out.rm1[t]))
                     status = ORC_STATUS_BUFFER_FULL;
+            if (jb->out.found > jb->out.cap) status = ORC_STATUS_BUFFER_FULL;
             free(jb->out.kind); free(jb->out.m); free(jb->out.n); free(jb->out.rm); free(jb->out.rm1);
         }
         free(jobs);
@@ -388,6 +398,18 @@ int orc_search_chunk(uint64_t index, uint64_t chunk_size, const uint64_t* primes
     }
     if (t_probe) *t_probe = now_s() - t1;
     return status;
+}
+
+/* chunked.py:307-359 -- all pairs whose n lies in chunk `index`'s domain, probing the
+ * earlier chunks j in [j_lo, j_hi) (the full search uses j_lo=0, j_hi=index). */
+int orc_search_chunk(uint64_t index, uint64_t chunk_size, const uint64_t* primes, size_t nprimes,
+                     uint64_t n_limit, int threads, uint64_t j_lo, uint64_t j_hi, uint64_t* slots,
+                     uint64_t table_size, uint64_t* vals, orc_pairs_t* out, double* t_build, double* t_probe) {
+    int status = orc_build_chunk(index, chunk_size, primes, nprimes, n_limit, slots, table_size, vals, out, t_build);
+    if (status == ORC_STATUS_TABLE_FULL) return status;
+    int st2 = orc_probe_chunks(index, chunk_size, primes, nprimes, threads, j_lo, j_hi, slots, table_size, vals,
+                               0, out, t_probe);
+    return status != ORC_STATUS_OK ? status : st2;
 }
 
 /* chunked.py:362-412 -- every chunk from resume_from on; pairs appended chunk by chunk. */

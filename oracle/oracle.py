@@ -82,6 +82,17 @@ def lib():
             ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_uint64, _u64p, ctypes.POINTER(_Pairs),
             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
         ]
+        L.orc_build_chunk.restype = ctypes.c_int
+        L.orc_build_chunk.argtypes = [
+            ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_uint64, _u64p, ctypes.c_uint64,
+            _u64p, ctypes.POINTER(_Pairs), ctypes.POINTER(ctypes.c_double),
+        ]
+        L.orc_probe_chunks.restype = ctypes.c_int
+        L.orc_probe_chunks.argtypes = [
+            ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64,
+            ctypes.c_uint64, _u64p, ctypes.c_uint64, _u64p, ctypes.c_uint64, ctypes.POINTER(_Pairs),
+            ctypes.POINTER(ctypes.c_double),
+        ]
         L.orc_run_full_chunked.restype = ctypes.c_int
         L.orc_run_full_chunked.argtypes = [
             ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int,
@@ -271,6 +282,36 @@ def search_chunk_sample(index: int, chunk_size: int, limit: int, threads: int, j
     if st not in (STATUS_OK, STATUS_BUFFER_FULL):
         raise RuntimeError(f"oracle search_chunk failed with status {st}")
     return ChunkSample(tb.value, tp.value, j_hi - j_lo, buf.rows())
+
+
+class ChunkTable:
+    """A built chunk table kept alive for repeated probe rounds (bench sampling):
+    chunked.py:326-333 (build) then chunked.py:335-356 (probe) on demand."""
+
+    def __init__(self, index: int, chunk_size: int, limit: int, primes: np.ndarray):
+        self.index, self.s, self.primes = index, chunk_size, primes
+        self.slots = np.zeros(table_size_for(chunk_size - 1), np.uint64)
+        self.vals = np.zeros(chunk_size, np.uint64)
+        buf = PairBuffers(4096)
+        t = ctypes.c_double(0)
+        st = lib().orc_build_chunk(index, chunk_size, _p(primes), primes.size, limit, _p(self.slots),
+                                   self.slots.size, _p(self.vals), ctypes.byref(buf.s), ctypes.byref(t))
+        if st not in (STATUS_OK, STATUS_BUFFER_FULL):
+            raise RuntimeError(f"oracle build failed with status {st}")
+        self.t_build = t.value
+        self.build_rows = buf.rows()
+
+    def probe(self, j_lo: int, j_hi: int, threads: int, sub_len: int = 0) -> tuple[float, list]:
+        """Probe with earlier chunks j in [j_lo, j_hi); sub_len > 0 probes only the first
+        sub_len values of each (a proportional sample of the same per-value work)."""
+        buf = PairBuffers(4096)
+        t = ctypes.c_double(0)
+        st = lib().orc_probe_chunks(self.index, self.s, _p(self.primes), self.primes.size, threads, j_lo, j_hi,
+                                    _p(self.slots), self.slots.size, _p(self.vals), sub_len, ctypes.byref(buf.s),
+                                    ctypes.byref(t))
+        if st not in (STATUS_OK, STATUS_BUFFER_FULL):
+            raise RuntimeError(f"oracle probe failed with status {st}")
+        return t.value, buf.rows()
 
 
 def num_chunks(limit: int, chunk_size: int) -> int:

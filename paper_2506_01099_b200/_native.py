@@ -28,7 +28,7 @@ KIND_FIRST, KIND_SECOND, KIND_BOTH = 1, 2, 3
 # Every symbol include/benelux_b200.h declares (tests check the library exports them all).
 EXPORTED_SYMBOLS = (
     "bnx_version", "bnx_last_error", "bnx_device_count", "bnx_ctx_create", "bnx_ctx_destroy",
-    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_primes_up_to", "bnx_sieve_radicals",
+    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_primes_up_to", "bnx_sieve_radicals",
     "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain",
     "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of",
 )
@@ -105,6 +105,8 @@ def load() -> ctypes.CDLL:
         L.bnx_ctx_destroy.argtypes = [vp]
         L.bnx_ctx_set_stream.argtypes = [vp, vp]
         L.bnx_ctx_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+        L.bnx_ctx_set_timing.argtypes = [vp, ctypes.c_int]
+        L.bnx_ctx_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
         L.bnx_primes_up_to.argtypes = [vp, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_sieve_radicals.argtypes = [
             vp, ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int, _u64p,
@@ -173,6 +175,16 @@ class Context:
         s = Stats()
         check(load().bnx_ctx_stats(self.handle, ctypes.byref(s)))
         return s.as_dict()
+
+    def set_timing(self, enabled: bool) -> None:
+        with self.lock:
+            check(load().bnx_ctx_set_timing(self.handle, int(bool(enabled))))
+
+    def timing(self) -> tuple[float, float]:
+        """(screen kernel ms, whole device pipeline ms) of the last search (CUDA events)."""
+        a, b = ctypes.c_float(0), ctypes.c_float(0)
+        check(load().bnx_ctx_timing(self.handle, ctypes.byref(a), ctypes.byref(b)))
+        return float(a.value), float(b.value)
 
     # -- primes ---------------------------------------------------------------------
     def primes_up_to(self, limit: int) -> np.ndarray:

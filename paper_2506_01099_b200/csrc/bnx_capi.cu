@@ -112,8 +112,6 @@ struct bnx_ctx {
     Tables screen_tab, sieve_tab, td_tab;
 
     DBuf<uint64_t> surv;
-    DBuf<BnxCand> cand;
-    DBuf<BnxMatch> match;
     DBuf<bnx_pair_t> pairs;
     DBuf<unsigned long long> ctr;
     DBuf<int> flags;
@@ -125,6 +123,11 @@ struct bnx_ctx {
     DBuf<uint64_t> t_npdiv;
     DBuf<int> t_over;
     DBuf<uint64_t> sieve_out;
+
+    // optional event timing of the pipeline
+    bool timing = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    float screen_ms = 0.f, pipeline_ms = 0.f;
 
     // the enqueued search
     bool q_valid = false;
@@ -261,8 +264,6 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
 
 int ensure_work(bnx_ctx* c) {
     if (!c->surv.p) TRY(c->surv.ensure(1 << 20));
-    if (!c->cand.p) TRY(c->cand.ensure(1 << 16));
-    if (!c->match.p) TRY(c->match.ensure(1 << 16));
     if (!c->pairs.p) TRY(c->pairs.ensure(1 << 14));
     TRY(c->ctr.ensure(CTR_N));
     TRY(c->flags.ensure(4));
@@ -284,14 +285,13 @@ int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     ScreenArgs sa{x_begin, nseg, n_first, n_last, t.small.p, (int)t.nsmall, t.large.p, (int)t.nlarge,
                   c->surv.p, c->surv.cap, c->ctr.p, c->flags.p};
     const int sgrid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->screen_blocks_per_sm);
+    if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     launch_screen(sa, sgrid, c->stream);
-    VerifyArgs va{c->surv.p, c->surv.cap, t.pdiv.p, t.npdiv, c->cand.p, c->cand.cap, c->ctr.p};
-    launch_verify(va, grid_for(c), c->stream);
-    EnumArgs ea{c->cand.p, c->cand.cap, kinds, c->match.p, c->match.cap, c->ctr.p};
-    launch_enumerate(ea, grid_for(c), c->stream);
-    FinalArgs fa{c->match.p, c->match.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap, c->ctr.p};
-    launch_finalize(fa, grid_for(c), c->stream);
+    if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
+    TailArgs ta{c->surv.p, c->surv.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap, c->ctr.p};
+    launch_tail(ta, grid_for(c), c->stream);
     CK(cudaGetLastError());
+    if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
     CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
     c->q_valid = true;
@@ -300,7 +300,7 @@ int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     c->q_kinds = kinds;
     c->stats = bnx_stats_t{};
     c->stats.integers = n_last - n_first + 1;
-    c->stats.kernel_launches = 4;
+    c->stats.kernel_launches = 2;
     return BNX_OK;
 }
 
@@ -322,8 +322,6 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
         const unsigned long long* h = c->h_ctr;
         bool again = false;
         if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
-        if (h[CTR_CAND] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_CAND] * 2)); again = true; }
-        if (h[CTR_MATCH] > c->match.cap) { TRY(c->match.ensure(h[CTR_MATCH] * 2)); again = true; }
         if (h[CTR_PAIRS] > c->pairs.cap) { TRY(c->pairs.ensure(h[CTR_PAIRS] * 2)); again = true; }
         if (again) {
             TRY(enqueue(c, c->q_first, c->q_last, c->q_kinds));
@@ -340,6 +338,10 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
         c->stats.residue_checks = h[CTR_CHECKS];
         c->stats.matches = h[CTR_MATCH];
         c->stats.pairs = np;
+        if (c->timing) {
+            CK(cudaEventElapsedTime(&c->screen_ms, c->ev[0], c->ev[1]));
+            CK(cudaEventElapsedTime(&c->pipeline_ms, c->ev[0], c->ev[2]));
+        }
         c->q_valid = false;
         return BNX_OK;
     }
@@ -413,8 +415,6 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->sieve_tab.release();
     c->td_tab.release();
     c->surv.release();
-    c->cand.release();
-    c->match.release();
     c->pairs.release();
     c->ctr.release();
     c->flags.release();
@@ -423,6 +423,8 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->t_npdiv.release();
     c->t_over.release();
     c->sieve_out.release();
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -450,6 +452,23 @@ int bnx_ctx_set_stream(bnx_ctx_t* c, void* stream) {
 int bnx_ctx_stats(const bnx_ctx_t* c, bnx_stats_t* out) {
     if (!c || !out) return fail(BNX_ERR_INVALID, "null argument");
     *out = c->stats;
+    return BNX_OK;
+}
+
+int bnx_ctx_set_timing(bnx_ctx_t* c, int enabled) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    TRY(activate(c));
+    if (enabled)
+        for (auto& e : c->ev)
+            if (!e) CK(cudaEventCreate(&e));
+    c->timing = enabled != 0;
+    return BNX_OK;
+}
+
+int bnx_ctx_timing(const bnx_ctx_t* c, float* screen_ms, float* pipeline_ms) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (screen_ms) *screen_ms = c->screen_ms;
+    if (pipeline_ms) *pipeline_ms = c->pipeline_ms;
     return BNX_OK;
 }
 

@@ -1,7 +1,7 @@
 // bnx_kernels.cu -- sm_100a kernels of the B200-native Benelux-pair search.
 //
 // Hot path:
-//   k_screen        on-chip segmented sieve of the quarter-bit log of the "surplus"
+//   k_screen        on-chip segmented sieve of the half-bit log of the "surplus"
 //                   s(x) = x / rad(x) over shared-memory tiles; flags every n whose
 //                   signature could collide:  rad(n) * rad(n+1) <= 2n   (Lemma).
 //                   Nothing per integer touches HBM.
@@ -144,9 +144,11 @@ __global__ void k_widen_primes(const uint32_t* in, uint64_t n, uint64_t* out) {
 // Progression tables: every q = p^e <= max_x, e >= 2 (odd p; p = 2 too when include_two),
 // split at `tile` into the per-tile list (q < tile) and the bucketed list.  Order inside a
 // list is irrelevant: hits commute.  Also the odd-prime exact-division table.
+// Screen weight of an odd prime: half-bits of log2 p rounded up (an over-estimate is safe:
+// the screen only needs A(x) >= 2 log2 s(x)).
 __device__ uint32_t prime_weight(uint32_t p) {
-    if (p == 2) return 4;
-    return (uint32_t)ceil(4.0 * log2((double)p) + 1e-7);
+    if (p == 2) return 2;
+    return (uint32_t)ceil(2.0 * log2((double)p) + 1e-7);
 }
 
 __global__ void k_build_tables(const uint32_t* primes, uint64_t np, uint64_t max_x, int include_two, uint32_t tile,
@@ -181,44 +183,73 @@ __global__ void k_build_tables(const uint32_t* primes, uint64_t np, uint64_t max
 }
 
 // ------------------------------------------------------------------------------------
-// THE SCREEN.  One CTA owns a segment of NT tiles of TILE integers; per tile the quarter-bit
-// log-surplus A(x) = sum over p^e | x, e >= 2, of w_p (w_p >= 4 log2 p) is accumulated as
-// packed bytes in shared memory with 32-bit shared atomics:
-//   * q = p^e < TILE:  strided per tile (block-wide for q < 64, warp-wide otherwise);
-//   * q >= TILE:       hits at most once per tile; enumerated once per segment into
-//                      per-tile shared-memory buckets.
-// p = 2 is exact from the bit position (ctz) in the scan.  A pair sum
-//   A(n) + A(n+1) >= 4 log2(s(n) s(n+1))  and  rad(n)rad(n+1) <= 2n  <=>  s(n)s(n+1) >= (n+1)/2,
-// so testing  A(n) + A(n+1) >= floor(4 log2(n+1)) - 5  never drops a candidate.
+// THE SCREEN.  One CTA owns a segment of NT tiles of TILE integers.  Per tile it builds,
+// in shared memory, one byte per integer:
+//     A(x) = sum over prime powers p^e | x (e >= 2) of w_p,   w_p = ceil(2 log2 p) >= 2 log2 p
+// (half-bits of log2 s(x), s(x) = x / rad(x), rounded up; p = 2 is exact).  The bytes start
+// from the 2-adic part (written by the tile initialisation) and odd prime powers add in
+// with 32-bit shared atomics, in four classes by q = p^e:
+//   B  q < 64            block-wide stride (9, 25, 27, 49: 0.21 hits per integer)
+//   W  64 <= q < 2048    one warp per progression
+//   L  2048 <= q < TILE  one lane per progression (sorted by q, so a warp's lanes agree)
+//   G  q >= TILE         at most one hit per tile: enumerated once per segment into
+//                        per-tile shared-memory buckets, applied block-wide.
+// Since rad(n)rad(n+1) <= 2n  <=>  s(n)s(n+1) >= (n+1)/2, every pair candidate satisfies
+//     A(n) + A(n+1) >= 2 log2(n+1) - 2 >= floor(2 log2(n+1)) - 2,
+// tested four integers per 32-bit word (SWAR; A(x) <= 108 < 128 so byte sums never carry),
+// after a one-AND pre-test on the high bits of the pair sums of 16 integers.
 template <int TILE, int NT, int THREADS, int BCAP, int MAXS>
-__global__ void __launch_bounds__(THREADS) k_screen(ScreenArgs a) {
+__global__ void __launch_bounds__(THREADS, 2) k_screen(ScreenArgs a) {
     constexpr int NW = THREADS / 32;
     constexpr uint32_t SEG = (uint32_t)TILE * NT;
     constexpr int WORDS = TILE / 4;
+    constexpr int GROUPS = WORDS / 4;  // 16 integers each
+    constexpr int GPT = GROUPS / THREADS;
+    static_assert(GROUPS % THREADS == 0, "scan: whole groups per thread");
+    static_assert(THREADS <= 1024 && (WORDS & (WORDS - 1)) == 0, "geometry");
     extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* acc = smem;                    // WORDS + 4 (the tile plus 4 integers of the next one)
+    uint32_t* acc = smem;                    // WORDS + 4 (the tile, then the next tile's first word group)
     uint32_t* bcnt = acc + WORDS + 4;        // NT
-    uint32_t* bent = bcnt + NT;              // NT * BCAP: (loc | w << 16)
-    uint32_t* s_q = bent + NT * BCAP;        // MAXS
+    uint32_t* bent = bcnt + NT;              // NT * BCAP: (loc | w << 17)
+    uint32_t* s_q = bent + NT * BCAP;        // MAXS, classes B | W | L in ascending q
     uint32_t* s_w = s_q + MAXS;
     uint32_t* s_tm = s_w + MAXS;
     uint32_t* s_off = s_tm + MAXS;
+    uint64_t* s_rc = (uint64_t*)(s_off + MAXS);  // MAXS reciprocals
+    __shared__ int s_cls[3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nsmall = a.nsmall;
-    for (int j = tid; j < nsmall; j += THREADS) {
-        uint32_t q = (uint32_t)a.small[j].q;
-        s_q[j] = q;
-        s_w[j] = a.small[j].w;
-        s_tm[j] = (uint32_t)TILE % q;
+    if (tid == 0) {
+        // sort the per-tile progressions by q (insertion sort, <= MAXS entries, once per launch)
+        for (int j = 0; j < nsmall; ++j) {
+            const BnxProg pr = a.small[j];
+            int k = j;
+            while (k > 0 && s_q[k - 1] > (uint32_t)pr.q) {
+                s_q[k] = s_q[k - 1]; s_w[k] = s_w[k - 1]; s_rc[k] = s_rc[k - 1];
+                --k;
+            }
+            s_q[k] = (uint32_t)pr.q; s_w[k] = pr.w; s_rc[k] = pr.recip;
+        }
+        int nb = 0, nw = 0;
+        while (nb < nsmall && s_q[nb] < 64) ++nb;
+        while (nb + nw < nsmall && s_q[nb + nw] < 2048) ++nw;
+        s_cls[0] = nb; s_cls[1] = nw; s_cls[2] = nsmall - nb - nw;
     }
+    __syncthreads();
+    for (int j = tid; j < nsmall; j += THREADS) s_tm[j] = (uint32_t)TILE % s_q[j];
+    const int nB = s_cls[0], nWp = s_cls[1], nL = s_cls[2];
+    // 2-adic half-bits 2(v2(x) - 1) of x = tile0 + 4j for the first word of each of this
+    // thread's groups (j = 4i, i = tid + k*THREADS): tile0 is a multiple of TILE > 4j, so
+    // v2(x) = 2 + v2(j) and the value is 2*ffs(j), the same for every k unless tid == 0.
+    const uint32_t c_grp = 2u * (uint32_t)__ffs(4 * (tid ? tid : THREADS));
 
     for (uint64_t seg = blockIdx.x; seg < a.nseg; seg += gridDim.x) {
         const uint64_t seg0 = a.x_begin + seg * SEG;
         __syncthreads();
         for (int j = tid; j < NT; j += THREADS) bcnt[j] = 0;
         for (int j = tid; j < nsmall; j += THREADS) {
-            uint64_t o = bnx_first_offset(seg0, s_q[j], a.small[j].recip);
+            uint64_t o = bnx_first_offset(seg0, s_q[j], s_rc[j]);
             if (seg0 == 0 && o == 0) o = s_q[j];  // never sieve x = 0
             s_off[j] = (uint32_t)o;
         }
@@ -229,7 +260,7 @@ __global__ void __launch_bounds__(THREADS) k_screen(ScreenArgs a) {
             if (seg0 == 0 && o == 0) o = pr.q;
             for (; o < SEG + 4; o += pr.q) {
                 const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
-                const uint32_t ent = pr.w << 16;
+                const uint32_t ent = pr.w << 17;  // loc needs 17 bits: TILE + 4 > 2^16
                 if (t < NT) {
                     uint32_t k = atomicAdd(&bcnt[t], 1u);
                     if (k < BCAP) bent[t * BCAP + k] = loc | ent; else a.flags[0] = 1;
@@ -245,30 +276,46 @@ __global__ void __launch_bounds__(THREADS) k_screen(ScreenArgs a) {
         for (int t = 0; t < NT; ++t) {
             const uint64_t tile0 = seg0 + (uint64_t)t * TILE;
             if (tile0 > a.n_last) break;
-            for (int i = tid; i < WORDS + 4; i += THREADS) acc[i] = 0;
+            // ---- init with the 2-adic part
+#pragma unroll
+            for (int k = 0; k < GPT; ++k) {
+                const int i = tid + k * THREADS;
+                uint32_t c0 = c_grp;
+                if (tid == 0) c0 = k ? 2u * (uint32_t)__ffs(4 * i) : (tile0 ? 2u * (uint32_t)(bnx_ctz64(tile0) - 1) : 0u);
+                reinterpret_cast<uint4*>(acc)[i] = make_uint4(c0, 2u, 4u, 2u);
+            }
+            if (tid == 0)
+                reinterpret_cast<uint4*>(acc)[GROUPS] =
+                    make_uint4(2u * (uint32_t)(bnx_ctz64(tile0 + TILE) - 1), 2u, 4u, 2u);
             __syncthreads();
-            // small progressions
-            for (int j = 0; j < nsmall; ++j) {
-                const uint32_t q = s_q[j];
-                if (q >= 64) continue;
-                const uint32_t w = s_w[j];
+            // ---- class B: block-wide
+            for (int j = 0; j < nB; ++j) {
+                const uint32_t q = s_q[j], w = s_w[j];
                 for (uint32_t o = s_off[j] + tid * q; o < TILE + 4; o += THREADS * q)
                     atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
             }
-            for (int j = warp; j < nsmall; j += NW) {
-                const uint32_t q = s_q[j];
-                if (q < 64) continue;
-                const uint32_t w = s_w[j];
+            // ---- class W: warp per progression
+            for (int j = nB + warp; j < nB + nWp; j += NW) {
+                const uint32_t q = s_q[j], w = s_w[j];
                 for (uint32_t o = s_off[j] + lane * q; o < TILE + 4; o += 32 * q)
                     atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
             }
-            // bucketed large progressions of this tile
+            // ---- class L: lane per progression, on the highest warps
+            {
+                const int g = NW - 1 - warp;  // lane group
+                const int j = nB + nWp + g * 32 + lane;
+                if (g * 32 < nL && j < nsmall) {
+                    const uint32_t q = s_q[j], w = s_w[j];
+                    for (uint32_t o = s_off[j]; o < TILE + 4; o += q) atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
+                }
+            }
+            // ---- class G: this tile's bucket
             {
                 const uint32_t nb = min(bcnt[t], (uint32_t)BCAP);
                 for (uint32_t i = tid; i < nb; i += THREADS) {
                     const uint32_t e = bent[t * BCAP + i];
-                    const uint32_t loc = e & 0xFFFFu;
-                    atomicAdd(&acc[loc >> 2], (e >> 16) << ((loc & 3) << 3));
+                    const uint32_t loc = e & 0x1FFFFu;
+                    atomicAdd(&acc[loc >> 2], (e >> 17) << ((loc & 3) << 3));
                 }
             }
             __syncthreads();
@@ -277,35 +324,35 @@ __global__ void __launch_bounds__(THREADS) k_screen(ScreenArgs a) {
                 if (no < 0) no += (int)s_q[j];
                 s_off[j] = (uint32_t)no;
             }
-            // scan: 4 integers per word, pair sums in 16-bit lanes
-            const bool low = tile0 < 65536;
-            const uint32_t t_tile = low ? 0u : (uint32_t)max(0, bnx_floor4log2(tile0 + 1) - 5);
-            const uint32_t c_first = tile0 ? 4u * (uint32_t)(bnx_ctz64(tile0) - 1) : 0u;
-            const uint64_t next0 = tile0 + TILE;
-            const uint32_t c_next = 4u * (uint32_t)(bnx_ctz64(next0) - 1);
-            for (int j = tid; j < WORDS; j += THREADS) {
-                const uint64_t x0 = tile0 + 4u * (uint32_t)j;
-                const uint32_t tw = low ? (uint32_t)max(0, bnx_floor4log2(x0 + 1) - 5) : t_tile;
-                const uint32_t a0 = acc[j], a1 = acc[j + 1];
-                const uint32_t c0 = j ? 4u * (uint32_t)__ffs(j) : c_first;
-                const uint32_t c4 = (j + 1 < WORDS) ? 4u * (uint32_t)__ffs(j + 1) : c_next;
-                const uint32_t sh = __funnelshift_r(a0, a1, 8);
-                const uint32_t ev = (a0 & 0x00FF00FFu) + (sh & 0x00FF00FFu) + c0;
-                const uint32_t od = ((a0 >> 8) & 0x00FF00FFu) + ((sh >> 8) & 0x00FF00FFu) + (c4 << 16);
-                const uint32_t bias = (0x8000u - tw) * 0x00010001u;
-                const uint32_t he = (ev + bias) & 0x80008000u, ho = (od + bias) & 0x80008000u;
-                if (he | ho) {
-                    uint64_t cand[4];
-                    int nc = 0;
-                    if (he & 0x8000u) cand[nc++] = x0;
-                    if (ho & 0x8000u) cand[nc++] = x0 + 1;
-                    if (he & 0x80000000u) cand[nc++] = x0 + 2;
-                    if (ho & 0x80000000u) cand[nc++] = x0 + 3;
-                    for (int c = 0; c < nc; ++c) {
-                        const uint64_t n = cand[c];
-                        if (n >= a.n_first && n <= a.n_last) {
-                            unsigned long long k = atomicAdd(&a.ctr[0], 1ull);
-                            if (k < a.surv_cap) a.surv[k] = n;
+            // ---- scan
+            const bool low = tile0 < (1u << 20);
+            const int tt = max(0, bnx_floor2log2(tile0 + 1) - 2);
+            const uint32_t pre = tt >= 2 ? ((0xFFu << (31 - __clz(tt))) & 0xFFu) * 0x01010101u : 0xFFFFFFFFu;
+#pragma unroll
+            for (int k = 0; k < GPT; ++k) {
+                const int i = tid + k * THREADS;
+                const uint4 v = reinterpret_cast<const uint4*>(acc)[i];
+                const uint32_t nx = acc[4 * i + 4];
+                const uint32_t s0 = v.x + __funnelshift_r(v.x, v.y, 8);  // A(x) + A(x+1), 4 bytes
+                const uint32_t s1 = v.y + __funnelshift_r(v.y, v.z, 8);
+                const uint32_t s2 = v.z + __funnelshift_r(v.z, v.w, 8);
+                const uint32_t s3 = v.w + __funnelshift_r(v.w, nx, 8);
+                if ((s0 | s1 | s2 | s3) & pre) {  // rare: exact per-byte test
+                    const uint64_t g0 = tile0 + 16u * (uint32_t)i;
+                    const uint32_t tw = low ? (uint32_t)max(0, bnx_floor2log2(g0 + 1) - 2) : (uint32_t)tt;
+                    const uint32_t T4 = tw * 0x01010101u;
+                    const uint32_t sv[4] = {s0, s1, s2, s3};
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        uint32_t m = (((sv[w] | 0x80808080u) - T4) | sv[w]) & 0x80808080u;
+                        while (m) {
+                            const int b = (__ffs(m) - 1) >> 3;
+                            m &= m - 1;
+                            const uint64_t n = g0 + 4u * w + b;
+                            if (n >= a.n_first && n <= a.n_last) {
+                                unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
+                                if (slot < a.surv_cap) a.surv[slot] = n;
+                            }
                         }
                     }
                 }
@@ -317,21 +364,31 @@ __global__ void __launch_bounds__(THREADS) k_screen(ScreenArgs a) {
 
 // ------------------------------------------------------------------------------------
 // Exact rad(x) by warp-cooperative trial division over the odd-prime table (ascending).
-// Each lane owns primes j = lane (mod 32); the partial products of the primes and of the
-// prime powers dividing x are multiplied across the warp; the cofactor is prime or 1.
+// Each lane owns primes j = lane (mod 32), four loads in flight; the partial products of
+// the primes and of the prime powers dividing x are multiplied across the warp; the
+// remaining cofactor is 1 or a prime.  All 32 lanes must call it (warp-collective).
 __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_t npd) {
     const int lane = threadIdx.x & 31;
     const int tz = bnx_ctz64(x);
     const uint64_t y = x >> tz;
     uint64_t pr = 1, pp = 1;
-    for (uint64_t j = lane; j < npd; j += 32) {
-        const BnxPDiv d = pd[j];
-        if (d.p * d.p > y) break;
-        uint64_t t = y * d.inv;
-        if (t <= d.lim) {
-            pr *= d.p;
-            pp *= d.p;
-            while (t * d.inv <= d.lim) { t *= d.inv; pp *= d.p; }
+    bool go = true;
+    for (uint64_t j = lane; go && j < npd; j += 128) {
+        BnxPDiv d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t jj = j + 32u * u;
+            d[u] = jj < npd ? pd[jj] : BnxPDiv{0xFFFFFFFFull, 0, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (d[u].p * d[u].p > y) { go = false; break; }
+            uint64_t t = y * d[u].inv;
+            if (t <= d[u].lim) {
+                pr *= d[u].p;
+                pp *= d[u].p;
+                while (t * d[u].inv <= d[u].lim) { t *= d[u].inv; pp *= d[u].p; }
+            }
         }
     }
 #pragma unroll
@@ -343,68 +400,61 @@ __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_
     return (tz ? 2ull : 1ull) * pr * (cof > 1 ? cof : 1ull);
 }
 
-__global__ void k_verify(VerifyArgs a) {
+// The tail of the search, one warp per screen survivor n:
+//  1. key:  exact r0 = rad(n), r1 = rad(n+1); n is a candidate iff R = r0 r1 <= 2n.
+//  2. collision pass on the residue classes.  For a pair m < n with S_m = S_n,
+//       first kind:  rad(n), rad(n+1) both divide n - m      ->  m = n - tR      (t >= 1)
+//       second kind: rad(n), rad(n+1) both divide n + m + 1  ->  m = tR - n - 1
+//     so the lanes walk those t; m is kept iff rad(m), rad(m+1) equal the required
+//     radicals, tested exactly: rad(m) == r  <=>  r | m  and  m / r | r^inf (gcds).
+//  3. every kept m is verified by full radical comparison (rad_warp of m and m+1) and
+//     classified as the reference does (signatures.py:67-81), then emitted.
+__global__ void __launch_bounds__(256) k_tail(TailArgs a) {
     const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const uint64_t cnt = min((uint64_t)a.ctr[0], a.surv_cap);
+    const int lane = threadIdx.x & 31;
+    const uint64_t cnt = min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
     for (uint64_t i = gw; i < cnt; i += nwarps) {
         const uint64_t n = a.surv[i];
         const uint64_t r0 = rad_warp(n, a.pdiv, a.npdiv);
         const uint64_t r1 = rad_warp(n + 1, a.pdiv, a.npdiv);
-        if ((threadIdx.x & 31) == 0 && __umul64hi(r0, r1) == 0 && r0 * r1 <= 2 * n) {
-            unsigned long long k = atomicAdd(&a.ctr[1], 1ull);
-            if (k < a.cand_cap) a.cand[k] = BnxCand{n, r0, r1};
-        }
-    }
-}
-
-// Collision pass on the residue classes.  For a pair m < n with S_m = S_n:
-//   first kind  rad(n) | n-m and rad(n+1) | n-m  ->  R | n - m      (m = n - tR,  t >= 1)
-//   second kind rad(n) | n+m+1 and rad(n+1) | n+m+1 -> R | n + m + 1 (m = tR - n - 1)
-// Each m is accepted iff rad(m), rad(m+1) equal the required radicals, tested exactly:
-// rad(m) == r  <=>  r | m  and  m / r | r^inf.
-__global__ void k_enumerate(EnumArgs a) {
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    const uint64_t cnt = min((uint64_t)a.ctr[1], a.cand_cap);
-    for (uint64_t i = gw; i < cnt; i += nwarps) {
-        const BnxCand c = a.cand[i];
-        const uint64_t n = c.n, R = c.r0 * c.r1;
-        const uint64_t t1 = (a.kinds & 1u) ? (n - 1) / R : 0;                // m = n - tR >= 1
-        const uint64_t t0 = (n + 1) / R + 1, t2 = (2 * n) / R;                 // n+2 <= tR <= 2n
+        if (__umul64hi(r0, r1) != 0 || r0 * r1 > 2 * n) continue;  // warp-uniform
+        const uint64_t R = r0 * r1;
+        const uint64_t t1 = (a.kinds & 1u) ? (n - 1) / R : 0;            // m = n - tR >= 1
+        const uint64_t t0 = (n + 1) / R + 1, t2 = (2 * n) / R;             // n + 2 <= tR <= 2n
         const uint64_t c2 = ((a.kinds & 2u) && t2 >= t0) ? t2 - t0 + 1 : 0;
         const uint64_t total = t1 + c2;
-        if (lane == 0 && total) atomicAdd(&a.ctr[2], (unsigned long long)total);
-        for (uint64_t k = lane; k < total; k += 32) {
-            uint64_t m, ra, rb;
-            uint32_t kind;
-            if (k < t1) { m = n - (k + 1) * R; ra = c.r0; rb = c.r1; kind = 1; }
-            else { m = (t0 + (k - t1)) * R - n - 1; ra = c.r1; rb = c.r0; kind = 2; }
-            // rad(m) == ra and rad(m+1) == rb
-            if (m % ra == 0 && (m + 1) % rb == 0 && bnx_supported_by(m / ra, ra) && bnx_supported_by((m + 1) / rb, rb)) {
-                unsigned long long s = atomicAdd(&a.ctr[3], 1ull);
-                if (s < a.match_cap) a.match[s] = BnxMatch{m, n, kind, 0};
-            }
+        if (lane == 0) {
+            atomicAdd(&a.ctr[CTR_CAND], 1ull);
+            if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
         }
-    }
-}
-
-// Exact verification by full radical comparison + classification (signatures.py:67-81).
-__global__ void k_finalize(FinalArgs a) {
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const uint64_t cnt = min((uint64_t)a.ctr[3], a.match_cap);
-    for (uint64_t i = gw; i < cnt; i += nwarps) {
-        const BnxMatch mt = a.match[i];
-        const uint64_t rm = rad_warp(mt.m, a.pdiv, a.npdiv), rm1 = rad_warp(mt.m + 1, a.pdiv, a.npdiv);
-        const uint64_t rn = rad_warp(mt.n, a.pdiv, a.npdiv), rn1 = rad_warp(mt.n + 1, a.pdiv, a.npdiv);
-        int kind = 0;
-        if (rm == rn && rm1 == rn1) kind = 1;
-        else if (rm == rn1 && rm1 == rn) kind = 2;
-        if ((threadIdx.x & 31) == 0 && kind && (a.kinds & (1u << (kind - 1))) && mt.m >= 1 && mt.m < mt.n) {
-            unsigned long long s = atomicAdd(&a.ctr[4], 1ull);
-            if (s < a.pair_cap) a.pairs[s] = bnx_pair_t{mt.m, mt.n, rm, rm1, kind, 0};
+        for (uint64_t base = 0; base < total; base += 32) {
+            const uint64_t k = base + lane;
+            uint64_t m = 0;
+            bool ok = false;
+            if (k < total) {
+                uint64_t ra, rb;
+                if (k < t1) { m = n - (k + 1) * R; ra = r0; rb = r1; }
+                else { m = (t0 + (k - t1)) * R - n - 1; ra = r1; rb = r0; }
+                ok = m % ra == 0 && (m + 1) % rb == 0 && bnx_supported_by(m / ra, ra) && bnx_supported_by((m + 1) / rb, rb);
+            }
+            uint32_t bal = __ballot_sync(0xffffffffu, ok);
+            while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
+                const uint64_t rm = rad_warp(mm, a.pdiv, a.npdiv), rm1 = rad_warp(mm + 1, a.pdiv, a.npdiv);
+                int kind = 0;
+                if (rm == r0 && rm1 == r1) kind = 1;
+                else if (rm == r1 && rm1 == r0) kind = 2;
+                if (lane == 0) {
+                    atomicAdd(&a.ctr[CTR_MATCH], 1ull);
+                    if (kind && (a.kinds & (1u << (kind - 1))) && mm >= 1 && mm < n) {
+                        unsigned long long s = atomicAdd(&a.ctr[CTR_PAIRS], 1ull);
+                        if (s < a.pair_cap) a.pairs[s] = bnx_pair_t{mm, n, rm, rm1, kind, 0};
+                    }
+                }
+            }
         }
     }
 }
@@ -546,7 +596,8 @@ __global__ void k_trial_division(uint64_t start, uint64_t length, const BnxPDiv*
 // ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
 size_t screen_smem_bytes() {
-    return sizeof(uint32_t) * ((size_t)(SCREEN_TILE / 4 + 4) + SCREEN_NT + (size_t)SCREEN_NT * SCREEN_BCAP + 4 * SCREEN_MAXS);
+    return sizeof(uint32_t) * ((size_t)(SCREEN_TILE / 4 + 4) + SCREEN_NT + (size_t)SCREEN_NT * SCREEN_BCAP + 4 * SCREEN_MAXS) +
+           sizeof(uint64_t) * SCREEN_MAXS;
 }
 size_t sieve_smem_bytes() {
     return sizeof(unsigned long long) * ((size_t)SIEVE_TILE + (size_t)SIEVE_NT * SIEVE_BCAP + SIEVE_MAXS) +
@@ -568,9 +619,7 @@ void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st) {
     k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>
         <<<grid, SIEVE_THREADS, sieve_smem_bytes(), st>>>(a);
 }
-void launch_verify(const VerifyArgs& a, int grid, cudaStream_t st) { k_verify<<<grid, 256, 0, st>>>(a); }
-void launch_enumerate(const EnumArgs& a, int grid, cudaStream_t st) { k_enumerate<<<grid, 256, 0, st>>>(a); }
-void launch_finalize(const FinalArgs& a, int grid, cudaStream_t st) { k_finalize<<<grid, 256, 0, st>>>(a); }
+void launch_tail(const TailArgs& a, int grid, cudaStream_t st) { k_tail<<<grid, 256, 0, st>>>(a); }
 
 void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st) {
     if (ls + 1 > 48 * 1024) cudaFuncSetAttribute(k_base_primes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ls + 1));

@@ -8,13 +8,13 @@
 
 namespace bnx {
 
-// Screen geometry: a tile is 32768 integers (one byte each, 32 KB of shared memory), a
+// Screen geometry: a tile is 65536 integers (one byte each, 64 KB of shared memory), a
 // segment is SCREEN_NT tiles; progressions q >= SCREEN_TILE hit a tile at most once and go
-// through per-tile buckets of SCREEN_BCAP entries (expected ~40 per tile).
-constexpr int SCREEN_TILE = 32768;
-constexpr int SCREEN_NT = 32;
-constexpr int SCREEN_THREADS = 512;
-constexpr int SCREEN_BCAP = 128;
+// through per-tile buckets of SCREEN_BCAP entries (expected ~60 per tile).
+constexpr int SCREEN_TILE = 65536;
+constexpr int SCREEN_NT = 16;
+constexpr int SCREEN_THREADS = 1024;
+constexpr int SCREEN_BCAP = 224;
 constexpr int SCREEN_MAXS = 160;
 
 // Exact radical sieve geometry: 4096 u64 slots per tile (32 KB).
@@ -41,28 +41,9 @@ struct ScreenArgs {
     int* flags;  // [0] bucket overflow
 };
 
-struct VerifyArgs {
+struct TailArgs {
     const uint64_t* surv;
     uint64_t surv_cap;
-    const BnxPDiv* pdiv;
-    uint64_t npdiv;
-    BnxCand* cand;
-    uint64_t cand_cap;
-    unsigned long long* ctr;
-};
-
-struct EnumArgs {
-    const BnxCand* cand;
-    uint64_t cand_cap;
-    uint32_t kinds;
-    BnxMatch* match;
-    uint64_t match_cap;
-    unsigned long long* ctr;
-};
-
-struct FinalArgs {
-    const BnxMatch* match;
-    uint64_t match_cap;
     const BnxPDiv* pdiv;
     uint64_t npdiv;
     uint32_t kinds;
@@ -88,9 +69,7 @@ const void* screen_kernel();
 const void* sieve_kernel();
 void launch_screen(const ScreenArgs& a, int grid, cudaStream_t st);
 void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st);
-void launch_verify(const VerifyArgs& a, int grid, cudaStream_t st);
-void launch_enumerate(const EnumArgs& a, int grid, cudaStream_t st);
-void launch_finalize(const FinalArgs& a, int grid, cudaStream_t st);
+void launch_tail(const TailArgs& a, int grid, cudaStream_t st);
 void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st);
 void launch_prime_seg(uint64_t lo, uint64_t hi, const uint32_t* base, uint32_t nbase, uint32_t* counts,
                       const uint64_t* offsets, uint32_t* out, uint64_t nblocks, cudaStream_t st);

@@ -65,8 +65,15 @@ BNX_D int bnx_floor4log2(uint64_t v) {
     return 4 * e + (m >= 0x9837f0518db8a970ull) + (m >= 0xb504f333f9de6485ull) + (m >= 0xd744fccad69d6af5ull);
 }
 
+// floor(2 * log2(v)) for v >= 1, exact (constant = ceil(2^63.5)).
+BNX_D int bnx_floor2log2(uint64_t v) {
+    int lz = __clzll((long long)v);
+    uint64_t m = v << lz;
+    return 2 * (63 - lz) + (m >= 0xb504f333f9de6485ull);
+}
+
 // A prime power progression q = p^e (e >= 2) of the sieve, with its reciprocal and the
-// screen weight w = ceil(4 log2 p) (quarter-bits of log2 p, rounded up).
+// screen weight w = ceil(2 log2 p) (half-bits of log2 p, rounded up).
 struct BnxProg {
     uint64_t q;
     uint64_t recip;

@@ -22,7 +22,7 @@ DEFAULT_MEMORY_BUDGET = 14 * 2**30
 
 # Fixed device work buffers of one search context (survivors, candidates, matches, pairs,
 # counters) and bytes per prime-table entry (prime, progression, exact-division constants).
-DEVICE_WORK_BYTES = (1 << 20) * 8 + (1 << 16) * (24 + 24) + (1 << 14) * 40 + 4096
+DEVICE_WORK_BYTES = (1 << 20) * 8 + (1 << 14) * 40 + 4096
 DEVICE_BYTES_PER_PRIME = 4 + 24 + 24
 
 
