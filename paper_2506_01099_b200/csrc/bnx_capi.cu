@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -82,12 +83,15 @@ struct Tables {
     uint64_t gen = ~0ull;
     DBuf<BnxProg> small, large;
     DBuf<BnxPDiv> pdiv;
+    DBuf<uint32_t> items;
+    int nitems = 0;
     uint32_t nsmall = 0;
     uint64_t nlarge = 0, npdiv = 0;
     void release() {
         small.release();
         large.release();
         pdiv.release();
+        items.release();
         gen = ~0ull;
     }
 };
@@ -100,6 +104,8 @@ struct bnx_ctx {
     bool own_stream = false;
     int num_sms = 148;
     int screen_blocks_per_sm = 1;
+    int screen_v = 0;
+    int screen_skip = 0;  // profiling only
     int sieve_blocks_per_sm = 1;
 
     // prime table (device u32 + host mirror)
@@ -218,6 +224,26 @@ int ensure_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
     return gen_primes(c, lim);
 }
 
+// Work items of the screen's per-tile progressions (q < tile, sorted by q): a progression
+// with q < 2048 is split into R interleaved items of about ITEM_HITS hits per tile; the
+// rest go 32 progressions per item (one per lane).  Items are ordered by decreasing hits so
+// the snake deal in k_screen balances the warps.  Encoding: j | r << 8 | R << 16 | packed << 31.
+std::vector<uint32_t> build_items(const std::vector<BnxProg>& small, uint32_t tile) {
+    constexpr uint32_t ITEM_HITS = 32 * 12;
+    std::vector<std::pair<uint32_t, uint32_t>> v;  // (cost, item)
+    size_t j = 0;
+    for (; j < small.size() && small[j].q < 2048; ++j) {
+        const uint32_t hits = tile / (uint32_t)small[j].q;
+        const uint32_t R = std::max(1u, (hits + ITEM_HITS / 2) / ITEM_HITS);
+        for (uint32_t r = 0; r < R; ++r) v.push_back({hits / R, (uint32_t)j | (r << 8) | (R << 16)});
+    }
+    for (; j < small.size(); j += 32) v.push_back({tile / (uint32_t)small[j].q, (uint32_t)j | (1u << 31)});
+    std::stable_sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<uint32_t> out;
+    for (auto& e : v) out.push_back(e.second);
+    return out;
+}
+
 int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_t tile) {
     if (t.gen == c->gen && t.max_x == max_x && t.include_two == include_two && t.tile == tile) return BNX_OK;
     const uint64_t root = isqrt_u64(max_x);
@@ -225,7 +251,7 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
     const uint64_t cb = icbrt_u64(max_x);
     const uint64_t npc = (uint64_t)(std::upper_bound(c->h_primes.begin(), c->h_primes.end(), (uint32_t)std::min<uint64_t>(cb, 0xFFFFFFFFull)) - c->h_primes.begin());
     const uint64_t large_cap = np + 63 * npc + 64;
-    const uint32_t small_cap = (uint32_t)(tile == (uint32_t)SCREEN_TILE ? SCREEN_MAXS : SIEVE_MAXS);
+    const uint32_t small_cap = (uint32_t)(tile == (uint32_t)SIEVE_TILE ? SIEVE_MAXS : SCREEN_MAXS);
     TRY(t.small.ensure(small_cap));
     TRY(t.large.ensure(large_cap));
     TRY(t.pdiv.ensure(np + 1));
@@ -252,6 +278,20 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
     CK(cudaMemcpyAsync(&over, c->t_over.p, sizeof(over), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (over) return fail(BNX_ERR_CUDA, "progression table overflow");
+    // per-tile progressions sorted by q, and the screen's work items (see k_screen)
+    if (ns > small_cap) return fail(BNX_ERR_CUDA, "too many small progressions");
+    std::vector<BnxProg> hs(ns);
+    if (ns) {
+        CK(cudaMemcpy(hs.data(), t.small.p, sizeof(BnxProg) * ns, cudaMemcpyDeviceToHost));
+        std::sort(hs.begin(), hs.end(), [](const BnxProg& x, const BnxProg& y) { return x.q < y.q; });
+        CK(cudaMemcpy(t.small.p, hs.data(), sizeof(BnxProg) * ns, cudaMemcpyHostToDevice));
+    }
+    std::vector<uint32_t> items = build_items(hs, tile);
+    if (items.size() > 2 * (size_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many screen work items");
+    TRY(t.items.ensure(items.size() + 1));
+    if (!items.empty())
+        CK(cudaMemcpy(t.items.p, items.data(), sizeof(uint32_t) * items.size(), cudaMemcpyHostToDevice));
+    t.nitems = (int)items.size();
     t.nsmall = ns;
     t.nlarge = nl;
     t.npdiv = npd;
@@ -277,16 +317,17 @@ int grid_for(bnx_ctx* c) { return c->num_sms * 4; }
 int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     Tables& t = c->screen_tab;
     TRY(ensure_work(c));
-    const uint64_t SEG = (uint64_t)SCREEN_TILE * SCREEN_NT;
-    const uint64_t x_begin = n_first / SCREEN_TILE * SCREEN_TILE;
+    const ScreenVariant& sv = screen_variant(c->screen_v);
+    const uint64_t SEG = (uint64_t)sv.tile * sv.nt;
+    const uint64_t x_begin = n_first / sv.tile * sv.tile;
     const uint64_t nseg = (n_last - x_begin + 1 + SEG - 1) / SEG;
     CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
     ScreenArgs sa{x_begin, nseg, n_first, n_last, t.small.p, (int)t.nsmall, t.large.p, (int)t.nlarge,
-                  c->surv.p, c->surv.cap, c->ctr.p, c->flags.p};
+                  t.items.p, t.nitems, c->surv.p, c->surv.cap, c->ctr.p, c->flags.p, c->screen_skip};
     const int sgrid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->screen_blocks_per_sm);
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
-    launch_screen(sa, sgrid, c->stream);
+    sv.launch(sa, sgrid, c->stream);
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
     TailArgs ta{c->surv.p, c->surv.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap, c->ctr.p};
     launch_tail(ta, grid_for(c), c->stream);
@@ -308,7 +349,7 @@ int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint6
     if (max_x >= (1ull << 42)) return fail(BNX_ERR_RANGE, "search bound must be below 2^42");
     const uint64_t need = isqrt_u64(max_x);
     TRY(ensure_primes(c, primes, np, plimit, need));
-    TRY(build_tables(c, c->screen_tab, max_x, 0, SCREEN_TILE));
+    TRY(build_tables(c, c->screen_tab, max_x, 0, (uint32_t)screen_variant(c->screen_v).tile));
     if (c->screen_tab.nsmall > (uint32_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     return BNX_OK;
 }
@@ -393,10 +434,17 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-    CK(cudaFuncSetAttribute(screen_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_smem_bytes()));
+    if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
+    if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
+        const int v = std::atoi(env);
+        if (v >= 0 && v < screen_variant_count()) c->screen_v = v;
+    }
+    {
+        const ScreenVariant& sv = screen_variant(c->screen_v);
+        CK(cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sv.smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->screen_blocks_per_sm, sv.fn, sv.threads, sv.smem));
+    }
     CK(cudaFuncSetAttribute(sieve_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sieve_smem_bytes()));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->screen_blocks_per_sm, screen_kernel(), SCREEN_THREADS,
-                                                     screen_smem_bytes()));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_blocks_per_sm, sieve_kernel(), SIEVE_THREADS,
                                                      sieve_smem_bytes()));
     c->screen_blocks_per_sm = std::max(1, c->screen_blocks_per_sm);

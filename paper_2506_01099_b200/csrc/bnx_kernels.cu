@@ -188,57 +188,52 @@ __global__ void k_build_tables(const uint32_t* primes, uint64_t np, uint64_t max
 //     A(x) = sum over prime powers p^e | x (e >= 2) of w_p,   w_p = ceil(2 log2 p) >= 2 log2 p
 // (half-bits of log2 s(x), s(x) = x / rad(x), rounded up; p = 2 is exact).  The bytes start
 // from the 2-adic part (written by the tile initialisation) and odd prime powers add in
-// with 32-bit shared atomics, in four classes by q = p^e:
-//   B  q < 64            block-wide stride (9, 25, 27, 49: 0.21 hits per integer)
-//   W  64 <= q < 2048    one warp per progression
-//   L  2048 <= q < TILE  one lane per progression (sorted by q, so a warp's lanes agree)
-//   G  q >= TILE         at most one hit per tile: enumerated once per segment into
-//                        per-tile shared-memory buckets, applied block-wide.
+// with 32-bit shared atomics:
+//   * q = p^e < 2048: "work items" of up to ITEM_HITS hits each (a progression with many
+//     hits per tile is split into R interleaved items), dealt to the warps in decreasing
+//     size so every warp carries the same load into the barrier.  A lane's stride 32*R*q is
+//     a multiple of 4, so its byte lane (and the shifted weight) never changes: the inner
+//     loop is one add, one shared atomic, one compare.
+//   * 2048 <= q < TILE: one lane per progression (items of 32 progressions, sorted by q).
+//   * q >= TILE: at most one hit per tile: enumerated once per segment into per-tile
+//     shared-memory buckets and applied block-wide.
 // Since rad(n)rad(n+1) <= 2n  <=>  s(n)s(n+1) >= (n+1)/2, every pair candidate satisfies
 //     A(n) + A(n+1) >= 2 log2(n+1) - 2 >= floor(2 log2(n+1)) - 2,
 // tested four integers per 32-bit word (SWAR; A(x) <= 108 < 128 so byte sums never carry),
 // after a one-AND pre-test on the high bits of the pair sums of 16 integers.
-template <int TILE, int NT, int THREADS, int BCAP, int MAXS>
-__global__ void __launch_bounds__(THREADS, 2) k_screen(ScreenArgs a) {
+template <int TILE, int NT, int THREADS, int BCAP, int MAXS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
     constexpr int NW = THREADS / 32;
     constexpr uint32_t SEG = (uint32_t)TILE * NT;
     constexpr int WORDS = TILE / 4;
     constexpr int GROUPS = WORDS / 4;  // 16 integers each
     constexpr int GPT = GROUPS / THREADS;
     static_assert(GROUPS % THREADS == 0, "scan: whole groups per thread");
-    static_assert(THREADS <= 1024 && (WORDS & (WORDS - 1)) == 0, "geometry");
+    static_assert((WORDS & (WORDS - 1)) == 0, "geometry");
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* acc = smem;                    // WORDS + 4 (the tile, then the next tile's first word group)
     uint32_t* bcnt = acc + WORDS + 4;        // NT
     uint32_t* bent = bcnt + NT;              // NT * BCAP: (loc | w << 17)
-    uint32_t* s_q = bent + NT * BCAP;        // MAXS, classes B | W | L in ascending q
+    uint32_t* s_q = bent + NT * BCAP;        // MAXS, ascending q
     uint32_t* s_w = s_q + MAXS;
     uint32_t* s_tm = s_w + MAXS;
     uint32_t* s_off = s_tm + MAXS;
-    uint64_t* s_rc = (uint64_t*)(s_off + MAXS);  // MAXS reciprocals
-    __shared__ int s_cls[3];
+    uint32_t* s_item = s_off + MAXS;         // 2*MAXS items: j | r << 8 | R << 16 | lanepacked << 31
+    uint64_t* s_rc = (uint64_t*)(s_item + 2 * MAXS);  // MAXS reciprocals
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nsmall = a.nsmall;
-    if (tid == 0) {
-        // sort the per-tile progressions by q (insertion sort, <= MAXS entries, once per launch)
-        for (int j = 0; j < nsmall; ++j) {
-            const BnxProg pr = a.small[j];
-            int k = j;
-            while (k > 0 && s_q[k - 1] > (uint32_t)pr.q) {
-                s_q[k] = s_q[k - 1]; s_w[k] = s_w[k - 1]; s_rc[k] = s_rc[k - 1];
-                --k;
-            }
-            s_q[k] = (uint32_t)pr.q; s_w[k] = pr.w; s_rc[k] = pr.recip;
-        }
-        int nb = 0, nw = 0;
-        while (nb < nsmall && s_q[nb] < 64) ++nb;
-        while (nb + nw < nsmall && s_q[nb + nw] < 2048) ++nw;
-        s_cls[0] = nb; s_cls[1] = nw; s_cls[2] = nsmall - nb - nw;
+    // per-tile progressions (sorted by q on the host) and their work items (build_tables)
+    for (int j = tid; j < nsmall; j += THREADS) {
+        const BnxProg pr = a.small[j];
+        s_q[j] = (uint32_t)pr.q;
+        s_w[j] = pr.w;
+        s_rc[j] = pr.recip;
+        s_tm[j] = (uint32_t)TILE % (uint32_t)pr.q;
     }
+    for (int j = tid; j < a.nitems; j += THREADS) s_item[j] = a.items[j];
     __syncthreads();
-    for (int j = tid; j < nsmall; j += THREADS) s_tm[j] = (uint32_t)TILE % s_q[j];
-    const int nB = s_cls[0], nWp = s_cls[1], nL = s_cls[2];
+    const int nitems = a.nitems;
     // 2-adic half-bits 2(v2(x) - 1) of x = tile0 + 4j for the first word of each of this
     // thread's groups (j = 4i, i = tid + k*THREADS): tile0 is a multiple of TILE > 4j, so
     // v2(x) = 2 + v2(j) and the value is 2*ffs(j), the same for every k unless tid == 0.
@@ -254,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_screen(ScreenArgs a) {
             s_off[j] = (uint32_t)o;
         }
         __syncthreads();
-        for (int j = tid; j < a.nlarge; j += THREADS) {
+        for (int j = (a.skip & 16) ? a.nlarge : tid; j < a.nlarge; j += THREADS) {
             const BnxProg pr = a.large[j];
             uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip);
             if (seg0 == 0 && o == 0) o = pr.q;
@@ -277,41 +272,52 @@ __global__ void __launch_bounds__(THREADS, 2) k_screen(ScreenArgs a) {
             const uint64_t tile0 = seg0 + (uint64_t)t * TILE;
             if (tile0 > a.n_last) break;
             // ---- init with the 2-adic part
+            uint4* acc4 = reinterpret_cast<uint4*>(acc);
+            if (!(a.skip & 8)) {
 #pragma unroll
-            for (int k = 0; k < GPT; ++k) {
-                const int i = tid + k * THREADS;
-                uint32_t c0 = c_grp;
-                if (tid == 0) c0 = k ? 2u * (uint32_t)__ffs(4 * i) : (tile0 ? 2u * (uint32_t)(bnx_ctz64(tile0) - 1) : 0u);
-                reinterpret_cast<uint4*>(acc)[i] = make_uint4(c0, 2u, 4u, 2u);
+            for (int k = 0; k < GPT; ++k) acc4[tid + k * THREADS] = make_uint4(c_grp, 2u, 4u, 2u);
             }
-            if (tid == 0)
-                reinterpret_cast<uint4*>(acc)[GROUPS] =
-                    make_uint4(2u * (uint32_t)(bnx_ctz64(tile0 + TILE) - 1), 2u, 4u, 2u);
+            if (tid == 0) {
+#pragma unroll
+                for (int k = 0; k < GPT; ++k)
+                    acc4[k * THREADS].x = k ? 2u * (uint32_t)__ffs(4 * k * THREADS)
+                                            : (tile0 ? 2u * (uint32_t)(bnx_ctz64(tile0) - 1) : 0u);
+                acc4[GROUPS] = make_uint4(2u * (uint32_t)(bnx_ctz64(tile0 + TILE) - 1), 2u, 4u, 2u);
+            }
             __syncthreads();
-            // ---- class B: block-wide
-            for (int j = 0; j < nB; ++j) {
-                const uint32_t q = s_q[j], w = s_w[j];
-                for (uint32_t o = s_off[j] + tid * q; o < TILE + 4; o += THREADS * q)
-                    atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
-            }
-            // ---- class W: warp per progression
-            for (int j = nB + warp; j < nB + nWp; j += NW) {
-                const uint32_t q = s_q[j], w = s_w[j];
-                for (uint32_t o = s_off[j] + lane * q; o < TILE + 4; o += 32 * q)
-                    atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
-            }
-            // ---- class L: lane per progression, on the highest warps
-            {
-                const int g = NW - 1 - warp;  // lane group
-                const int j = nB + nWp + g * 32 + lane;
-                if (g * 32 < nL && j < nsmall) {
-                    const uint32_t q = s_q[j], w = s_w[j];
-                    for (uint32_t o = s_off[j]; o < TILE + 4; o += q) atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
+            // ---- progressions q < TILE: balanced work items
+            for (int round = 0; !(a.skip & 1); ++round) {
+                // snake order over the size-sorted items
+                const int it = round * NW + ((round & 1) ? NW - 1 - warp : warp);
+                if (it >= nitems) break;
+                const uint32_t e = s_item[it];
+                const int j = (int)(e & 0xFFu);
+                if (e >> 31) {  // lane-packed: one progression per lane
+                    const int jj = j + lane;
+                    if (jj < nsmall) {
+                        const uint32_t q = s_q[jj], w = s_w[jj];
+                        for (uint32_t o = s_off[jj]; o < TILE + 4; o += q) atomicAdd(&acc[o >> 2], w << ((o & 3) << 3));
+                    }
+                } else {
+                    const uint32_t r = (e >> 8) & 0xFFu, R = (e >> 16) & 0x7FFFu;
+                    const uint32_t q = s_q[j];
+                    const uint32_t o = s_off[j] + (r * 32u + (uint32_t)lane) * q;
+                    if (o < TILE + 4) {
+                        const uint32_t wsh = s_w[j] << ((o & 3) << 3);     // invariant: stride % 4 == 0
+                        const uint32_t step = (32u * R * q) >> 2;            // words
+                        const uint32_t lim = (TILE + 4 - (o & 3) + 3) >> 2;  // word bound for this byte lane
+                        uint32_t wd = o >> 2;
+                        for (; wd + step < lim; wd += 2 * step) {
+                            atomicAdd(&acc[wd], wsh);
+                            atomicAdd(&acc[wd + step], wsh);
+                        }
+                        if (wd < lim) atomicAdd(&acc[wd], wsh);
+                    }
                 }
             }
-            // ---- class G: this tile's bucket
+            // ---- q >= TILE: this tile's bucket
             {
-                const uint32_t nb = min(bcnt[t], (uint32_t)BCAP);
+                const uint32_t nb = (a.skip & 2) ? 0u : min(bcnt[t], (uint32_t)BCAP);
                 for (uint32_t i = tid; i < nb; i += THREADS) {
                     const uint32_t e = bent[t * BCAP + i];
                     const uint32_t loc = e & 0x1FFFFu;
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_screen(ScreenArgs a) {
             const int tt = max(0, bnx_floor2log2(tile0 + 1) - 2);
             const uint32_t pre = tt >= 2 ? ((0xFFu << (31 - __clz(tt))) & 0xFFu) * 0x01010101u : 0xFFFFFFFFu;
 #pragma unroll
-            for (int k = 0; k < GPT; ++k) {
+            for (int k = 0; k < ((a.skip & 4) ? 0 : GPT); ++k) {
                 const int i = tid + k * THREADS;
                 const uint4 v = reinterpret_cast<const uint4*>(acc)[i];
                 const uint32_t nx = acc[4 * i + 4];
@@ -595,26 +601,38 @@ __global__ void k_trial_division(uint64_t start, uint64_t length, const BnxPDiv*
 
 // ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
-size_t screen_smem_bytes() {
-    return sizeof(uint32_t) * ((size_t)(SCREEN_TILE / 4 + 4) + SCREEN_NT + (size_t)SCREEN_NT * SCREEN_BCAP + 4 * SCREEN_MAXS) +
-           sizeof(uint64_t) * SCREEN_MAXS;
-}
 size_t sieve_smem_bytes() {
     return sizeof(unsigned long long) * ((size_t)SIEVE_TILE + (size_t)SIEVE_NT * SIEVE_BCAP + SIEVE_MAXS) +
            sizeof(uint32_t) * ((size_t)SIEVE_NT + 4 * SIEVE_MAXS);
 }
 
-const void* screen_kernel() {
-    return (const void*)k_screen<SCREEN_TILE, SCREEN_NT, SCREEN_THREADS, SCREEN_BCAP, SCREEN_MAXS>;
-}
 const void* sieve_kernel() {
     return (const void*)k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>;
 }
 
-void launch_screen(const ScreenArgs& a, int grid, cudaStream_t st) {
-    k_screen<SCREEN_TILE, SCREEN_NT, SCREEN_THREADS, SCREEN_BCAP, SCREEN_MAXS>
-        <<<grid, SCREEN_THREADS, screen_smem_bytes(), st>>>(a);
+template <int TILE, int NT, int THREADS, int BCAP>
+constexpr size_t screen_smem() {
+    return sizeof(uint32_t) * ((size_t)(TILE / 4 + 4) + NT + (size_t)NT * BCAP + 6 * SCREEN_MAXS) +
+           sizeof(uint64_t) * SCREEN_MAXS;
 }
+template <int TILE, int NT, int THREADS, int BCAP, int MINB>
+void launch_screen_v(const ScreenArgs& a, int grid, cudaStream_t st) {
+    k_screen<TILE, NT, THREADS, BCAP, SCREEN_MAXS, MINB>
+        <<<grid, THREADS, screen_smem<TILE, NT, THREADS, BCAP>(), st>>>(a);
+}
+#define BNX_SCREEN_VARIANT(T, N, H, B, M)                                                               \
+    ScreenVariant{T, N, H, B, (const void*)k_screen<T, N, H, B, SCREEN_MAXS, M>, screen_smem<T, N, H, B>(), \
+                  launch_screen_v<T, N, H, B, M>}
+static const ScreenVariant kScreenVariants[] = {
+    BNX_SCREEN_VARIANT(32768, 32, 512, 128, 4),
+    BNX_SCREEN_VARIANT(32768, 32, 512, 128, 3),
+    BNX_SCREEN_VARIANT(32768, 32, 256, 128, 8),
+    BNX_SCREEN_VARIANT(16384, 64, 256, 96, 8),
+    BNX_SCREEN_VARIANT(65536, 16, 512, 224, 2),
+    BNX_SCREEN_VARIANT(16384, 64, 512, 96, 4),
+};
+int screen_variant_count() { return (int)(sizeof(kScreenVariants) / sizeof(kScreenVariants[0])); }
+const ScreenVariant& screen_variant(int i) { return kScreenVariants[i]; }
 void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st) {
     k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>
         <<<grid, SIEVE_THREADS, sieve_smem_bytes(), st>>>(a);

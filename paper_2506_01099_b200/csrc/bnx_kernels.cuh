@@ -8,13 +8,7 @@
 
 namespace bnx {
 
-// Screen geometry: a tile is 65536 integers (one byte each, 64 KB of shared memory), a
-// segment is SCREEN_NT tiles; progressions q >= SCREEN_TILE hit a tile at most once and go
-// through per-tile buckets of SCREEN_BCAP entries (expected ~60 per tile).
-constexpr int SCREEN_TILE = 65536;
-constexpr int SCREEN_NT = 16;
-constexpr int SCREEN_THREADS = 1024;
-constexpr int SCREEN_BCAP = 224;
+// Screen: per-tile progressions (q < tile) at most SCREEN_MAXS; geometry variants below.
 constexpr int SCREEN_MAXS = 160;
 
 // Exact radical sieve geometry: 4096 u64 slots per tile (32 KB).
@@ -35,10 +29,13 @@ struct ScreenArgs {
     int nsmall;
     const BnxProg* large;
     int nlarge;
+    const uint32_t* items;  // work items over `small` (sorted by q), see build_items
+    int nitems;
     uint64_t* surv;
     uint64_t surv_cap;
     unsigned long long* ctr;
     int* flags;  // [0] bucket overflow
+    int skip;    // profiling only (BNX_SCREEN_SKIP): 1 items, 2 buckets, 4 scan, 8 init, 16 segment setup
 };
 
 struct TailArgs {
@@ -63,11 +60,18 @@ struct SieveArgs {
     int* flags;
 };
 
-size_t screen_smem_bytes();
+// Compiled screen geometries (tile, tiles per segment, threads, bucket capacity); the
+// context picks one at creation (BNX_SCREEN_VARIANT, default 0).
+struct ScreenVariant {
+    int tile, nt, threads, bcap;
+    const void* fn;
+    size_t smem;
+    void (*launch)(const ScreenArgs&, int, cudaStream_t);
+};
+int screen_variant_count();
+const ScreenVariant& screen_variant(int i);
 size_t sieve_smem_bytes();
-const void* screen_kernel();
 const void* sieve_kernel();
-void launch_screen(const ScreenArgs& a, int grid, cudaStream_t st);
 void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st);
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st);
 void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st);
