@@ -363,6 +363,30 @@ def run_ours(args) -> None:
     if traffic and traffic.get("dram_bytes_per_integer") is not None:
         traffic_bytes = traffic["dram_bytes_per_integer"] * ints_local
 
+    # ---- secondary: the exact radical sieve (radical.py:109-124) materialising rad(x) as
+    # uint64 in HBM -- a write-bound kernel, 8 algorithmic bytes per integer
+    sieve = None
+    if rank == 0 and not args.no_sieve:
+        n_sieve = 1 << 30
+        out = torch.empty(n_sieve, dtype=torch.int64, device=dev)
+        ctx.sieve_radicals_dev(1, n_sieve, out.data_ptr())  # warm-up: tables
+        times = []
+        for k in range(3):
+            flush.fill_(k & 0xFF)
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream)
+            ctx.sieve_radicals_dev(1, n_sieve, out.data_ptr())
+            b_ev.record(stream)
+            b_ev.synchronize()
+            times.append(a_ev.elapsed_time(b_ev))
+        t_ms = min(times)
+        gbs = 8 * n_sieve / (t_ms / 1e3) / 1e9
+        sieve = {"kernel": "k_sieve_exact", "integers": n_sieve, "ms": t_ms, "achieved": gbs, "peak": peak,
+                 "unit": "GB/s", "frac": gbs / peak, "bound": "hbm",
+                 "bytes_per_integer": 8, "check_rad_2^30": int(out[-1].item())}
+        del out
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -413,6 +437,7 @@ def run_ours(args) -> None:
                 "screen_share_of_step": scr_ms / ms_local,
             },
             "cpu_baseline": cpu,
+            "sieve_roofline": sieve,
             "search_stats": stats,
             "wall_s_timed_region": wall,
         }
@@ -428,6 +453,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sieve", action="store_true", help="skip the secondary radical-sieve roofline")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -369,10 +369,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
-// Exact rad(x) by warp-cooperative trial division over the odd-prime table (ascending).
-// Each lane owns primes j = lane (mod 32), four loads in flight; the partial products of
-// the primes and of the prime powers dividing x are multiplied across the warp; the
-// remaining cofactor is 1 or a prime.  All 32 lanes must call it (warp-collective).
+// Exact rad(x) (x < 2^42) by warp-cooperative trial division over the odd-prime table up to
+// cbrt(x) only: afterwards the cofactor c has at most two prime factors, all > cbrt(x), so
+// c is 1, p, p^2 or p*q and rad(c) = isqrt(c) if c is a square, else c.  Each lane owns
+// primes j = lane (mod 32), four loads in flight; the partial products of the primes and of
+// the prime powers dividing x are multiplied across the warp.  Warp-collective.
 __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_t npd) {
     const int lane = threadIdx.x & 31;
     const int tz = bnx_ctz64(x);
@@ -384,11 +385,11 @@ __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const uint64_t jj = j + 32u * u;
-            d[u] = jj < npd ? pd[jj] : BnxPDiv{0xFFFFFFFFull, 0, 0};
+            d[u] = jj < npd ? pd[jj] : BnxPDiv{1ull << 21, 0, 0};  // sentinel: p^3 = 2^63 > y
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            if (d[u].p * d[u].p > y) { go = false; break; }
+            if (d[u].p * d[u].p * d[u].p > y) { go = false; break; }  // p <= 2^21: no overflow
             uint64_t t = y * d[u].inv;
             if (t <= d[u].lim) {
                 pr *= d[u].p;
@@ -402,8 +403,15 @@ __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_
         pr *= __shfl_xor_sync(0xffffffffu, pr, o);
         pp *= __shfl_xor_sync(0xffffffffu, pp, o);
     }
-    const uint64_t cof = y * bnx_inv64(pp);
-    return (tz ? 2ull : 1ull) * pr * (cof > 1 ? cof : 1ull);
+    const uint64_t c = y * bnx_inv64(pp);  // exact: pp | y, both odd
+    uint64_t rc = c;
+    if (c > 1) {
+        uint64_t s = (uint64_t)sqrt((double)c);
+        while (s * s > c) --s;
+        while ((s + 1) * (s + 1) <= c) ++s;
+        if (s * s == c) rc = s;
+    }
+    return (tz ? 2ull : 1ull) * pr * rc;
 }
 
 // The tail of the search, one warp per screen survivor n:

@@ -92,7 +92,7 @@ def main():
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
             lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) * 1e6:.1f} | {sum(v) / total:.1%} |")
     os.makedirs(args.out, exist_ok=True)
-    short = "screen" if "k_screen" in name else name.split("::")[-1].split("<")[0].split("(")[0]
+    short = "screen" if "k_screen" in name else name.split("::")[-1].split("<")[0].split("(")[0].split()[-1]
     with open(os.path.join(args.out, f"{args.tag}_ncu_{short}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     if short == "screen":
