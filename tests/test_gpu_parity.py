@@ -169,3 +169,18 @@ def test_errors():
         list(bp.run_full_chunked(2, 300))
     with pytest.raises(ValueError):
         list(bp.run_full_chunked(5000, 2))
+
+
+def test_reference_run_2p32_exact_rows():
+    """The unmodified reference's own run_full_chunked(2^32, 2^28) (tests/golden/
+    make_golden_2p32.py, 1430 s on 8 threads) against the device search: identical rows in
+    identical (chunk, n, m) order."""
+    import json
+    import os
+
+    from conftest import ROOT
+
+    ref = json.load(open(os.path.join(ROOT, "tests", "golden", "ref_pairs_2p32.json")))["rows"]
+    assert rows_of(bp.run_full_chunked(2**32, 2**28)) == ref
+    assert sorted(rows_of(bp.find_pairs_sorted(2**32)), key=lambda r: (r[1], r[2])) == \
+        sorted(ref, key=lambda r: (r[1], r[2]))

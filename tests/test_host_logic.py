@@ -222,3 +222,14 @@ def test_search_chunk_domain_logic(orc, monkeypatch, golden):
     with pytest.raises(ValueError):
         bp.search_chunk(5, 1000, bp.PrimeList(np.array([2], np.uint64), 10))
     assert bp.search_chunk(0, 100, None, n_limit=1) == []
+
+
+def test_reference_2p32_fixture_is_theorem_1(golden):
+    import json
+    import os
+
+    from conftest import ROOT
+
+    ref = json.load(open(os.path.join(ROOT, "tests", "golden", "ref_pairs_2p32.json")))["rows"]
+    exp = golden["expected_pairs_up_to"]["4294967296"]
+    assert sorted(map(tuple, ref)) == sorted(map(tuple, exp["first"] + exp["second"]))
