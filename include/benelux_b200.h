@@ -15,6 +15,7 @@
  *   bnx_search                  <- sort_search.py:37-91      find_pairs_sorted(limit, primes)
  *   bnx_search_domain           <- chunked.py:307-359        search_chunk(index, s, primes, n_limit)
  *                                  (+ chunked.py:362-412      run_full_chunked, one call per chunk)
+ *   bnx_brute_force             <- bruteforce.py:16-42       brute_force_pairs(limit) (_kernels.py:235-263)
  *   bnx_slot_of                 <- _kernels.py:115-123 /     _slot_of / commutative_hash
  *                                  chunked.py:93-109
  *   status codes                <- _kernels.py:17-19         STATUS_OK / TABLE_FULL / BUFFER_FULL
@@ -115,6 +116,10 @@ BNX_API int bnx_sieve_radicals_dev(bnx_ctx_t* ctx, uint64_t start, uint64_t leng
 
 /* _kernels.py:87-112: out[k] = rad(start + k) by per-integer trial division on the GPU. */
 BNX_API int bnx_radicals_trial_division(bnx_ctx_t* ctx, uint64_t start, uint64_t length, uint64_t* out);
+
+/* bruteforce.py:16-42 + _kernels.py:235-263: the quadratic scan over trial-division radicals,
+ * on the GPU (limit <= 2^22); rows sorted by (m, n).  An independent check of bnx_search. */
+BNX_API int bnx_brute_force(bnx_ctx_t* ctx, uint64_t limit, bnx_pair_t* out, size_t cap, size_t* found);
 
 /* sort_search.py:37-91: every pair m < n < limit of the kinds in kinds_mask.
  * Rows come back sorted by (m, n).  primes may be NULL (device-built). */

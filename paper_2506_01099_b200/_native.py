@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = (
     "bnx_version", "bnx_last_error", "bnx_device_count", "bnx_ctx_create", "bnx_ctx_destroy",
     "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_primes_up_to", "bnx_sieve_radicals",
     "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain",
-    "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of",
+    "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of", "bnx_brute_force",
 )
 
 
@@ -119,6 +119,8 @@ def load() -> ctypes.CDLL:
         ]
         L.bnx_search.argtypes = search_args
         L.bnx_search_domain.argtypes = [vp, ctypes.c_uint64] + search_args[1:]
+        L.bnx_brute_force.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(PairRow), ctypes.c_size_t,
+                                      ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_prepare.argtypes = [vp, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_uint64]
         L.bnx_search_enqueue.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32]
         L.bnx_search_collect.argtypes = [vp, ctypes.POINTER(PairRow), ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
@@ -245,6 +247,9 @@ class Context:
         return self._rows(
             lambda b, c, f: load().bnx_search_domain(self.handle, n_first, n_last, kinds, pp, np_, primes_limit, b, c, f)
         )
+
+    def brute_force(self, limit: int) -> np.ndarray:
+        return self._rows(lambda b, c, f: load().bnx_brute_force(self.handle, limit, b, c, f))
 
     def prepare(self, max_x: int, primes: np.ndarray | None = None, primes_limit: int = 0) -> None:
         keep, pp, np_ = _prime_args(primes)  # noqa: F841 (keeps the array alive)

@@ -600,6 +600,42 @@ int bnx_radicals_trial_division(bnx_ctx_t* c, uint64_t start, uint64_t length, u
     return BNX_OK;
 }
 
+int bnx_brute_force(bnx_ctx_t* c, uint64_t limit, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (limit < 3) return fail(BNX_ERR_INVALID, "limit must be >= 3");
+    if (limit > (1ull << 22)) return fail(BNX_ERR_RANGE, "brute force is limited to 2^22 (quadratic)");
+    TRY(activate(c));
+    TRY(ensure_primes(c, nullptr, 0, 0, isqrt_u64(limit)));
+    TRY(build_tables(c, c->td_tab, limit, 0, SIEVE_TILE));
+    DBuf<uint64_t> rads;
+    DBuf<bnx_pair_t> rows;
+    DBuf<unsigned long long> cnt;
+    TRY(rads.ensure(limit));
+    TRY(cnt.ensure(1));
+    launch_trial_division(1, limit, c->td_tab.pdiv.p, c->td_tab.npdiv, rads.p, c->num_sms * 8, c->stream);
+    uint64_t cap_dev = 4096;
+    unsigned long long n = 0;
+    for (;;) {
+        TRY(rows.ensure(cap_dev));
+        CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), c->stream));
+        launch_brute_force(rads.p, limit, rows.p, cap_dev, cnt.p, c->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&n, cnt.p, sizeof(n), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (n <= cap_dev) break;
+        cap_dev = n;
+    }
+    std::vector<bnx_pair_t> v(n);
+    if (n) CK(cudaMemcpy(v.data(), rows.p, sizeof(bnx_pair_t) * n, cudaMemcpyDeviceToHost));
+    rads.release();
+    rows.release();
+    cnt.release();
+    std::sort(v.begin(), v.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
+        return a.m != b.m ? a.m < b.m : a.n < b.n;
+    });
+    return emit(v, out, cap, found);
+}
+
 int bnx_prepare(bnx_ctx_t* c, uint64_t max_x, const uint64_t* primes, size_t nprimes, uint64_t primes_limit) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");
     TRY(activate(c));

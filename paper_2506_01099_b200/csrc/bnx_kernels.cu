@@ -608,6 +608,40 @@ __global__ void k_trial_division(uint64_t start, uint64_t length, const BnxPDiv*
 }
 
 // ------------------------------------------------------------------------------------
+// bruteforce.py:16-42 / _kernels.py:235-263 on the GPU: the quadratic reference scan, an
+// independent check of the search (no sieve, no screen, no residue classes).  rads[t] =
+// rad(t+1) for t < limit (from k_trial_division); a block owns 256 consecutive m and streams
+// all n > m through shared-memory tiles.
+__global__ void __launch_bounds__(256) k_brute_force(const uint64_t* __restrict__ rads, uint64_t limit,
+                                                     bnx_pair_t* out, uint64_t cap, unsigned long long* count) {
+    __shared__ uint64_t tile[2049];
+    const uint64_t m0 = 1 + (uint64_t)blockIdx.x * blockDim.x;
+    const uint64_t m = m0 + threadIdx.x;
+    const bool live = m + 1 < limit;
+    const uint64_t rm = live ? rads[m - 1] : 0, rm1 = live ? rads[m] : 0;
+    for (uint64_t n0 = m0 + 1; n0 < limit; n0 += 2048) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < 2049; i += blockDim.x) {  // rads of n0-1 .. n0+2047
+            const uint64_t t = n0 - 1 + i;
+            tile[i] = t < limit ? rads[t] : 0;
+        }
+        __syncthreads();
+        if (!live) continue;
+        const uint64_t nend = min(limit, n0 + 2048);
+        for (uint64_t n = max(n0, m + 1); n < nend; ++n) {
+            const uint64_t rn = tile[n - n0], rn1 = tile[n - n0 + 1];
+            int kind = 0;
+            if (rn == rm && rn1 == rm1) kind = 1;
+            else if (rn == rm1 && rn1 == rm) kind = 2;
+            if (kind) {
+                unsigned long long k = atomicAdd(count, 1ull);
+                if (k < cap) out[k] = bnx_pair_t{m, n, rm, rm1, kind, 0};
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
 size_t sieve_smem_bytes() {
     return sizeof(unsigned long long) * ((size_t)SIEVE_TILE + (size_t)SIEVE_NT * SIEVE_BCAP + SIEVE_MAXS) +
@@ -670,6 +704,11 @@ void launch_build_tables(const uint32_t* primes, uint64_t np, uint64_t max_x, in
                          int* overflow, cudaStream_t st) {
     k_build_tables<<<256, 256, 0, st>>>(primes, np, max_x, include_two, tile, small, nsmall, small_cap, large, nlarge,
                                         large_cap, pdiv, npdiv, overflow);
+}
+void launch_brute_force(const uint64_t* rads, uint64_t limit, bnx_pair_t* out, uint64_t cap,
+                        unsigned long long* count, cudaStream_t st) {
+    const uint64_t blocks = (limit + 255) / 256;
+    k_brute_force<<<(unsigned)blocks, 256, 0, st>>>(rads, limit, out, cap, count);
 }
 void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out,
                            int grid, cudaStream_t st) {

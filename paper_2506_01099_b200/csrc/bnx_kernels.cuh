@@ -84,6 +84,8 @@ void launch_build_tables(const uint32_t* primes, uint64_t np, uint64_t max_x, in
                          BnxProg* small, uint32_t* nsmall, uint32_t small_cap, BnxProg* large,
                          unsigned long long* nlarge, uint64_t large_cap, BnxPDiv* pdiv, uint64_t* npdiv,
                          int* overflow, cudaStream_t st);
+void launch_brute_force(const uint64_t* rads, uint64_t limit, bnx_pair_t* out, uint64_t cap,
+                        unsigned long long* count, cudaStream_t st);
 void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out,
                            int grid, cudaStream_t st);
 
