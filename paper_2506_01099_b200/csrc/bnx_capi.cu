@@ -554,7 +554,7 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
         const uint64_t len = std::min<uint64_t>(piece, length - off);
         uint64_t* dst = out_dev ? out_dev : c->sieve_out.p;
         SieveArgs sa{start + off, len, c->sieve_tab.small.p, (int)c->sieve_tab.nsmall, c->sieve_tab.large.p,
-                     c->sieve_tab.nlarge, fast, dst, c->flags.p};
+                     c->sieve_tab.nlarge, c->sieve_tab.items.p, c->sieve_tab.nitems, fast, dst, c->flags.p};
         const uint64_t nseg = (len + SEG - 1) / SEG;
         const int grid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->sieve_blocks_per_sm);
         launch_sieve(sa, grid, c->stream);

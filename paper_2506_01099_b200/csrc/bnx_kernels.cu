@@ -488,28 +488,28 @@ __device__ __forceinline__ void div_slot(unsigned long long* s, uint64_t inv, bo
 }
 
 template <int TILE, int NT, int THREADS, int BCAP, int MAXS>
-__global__ void __launch_bounds__(THREADS) k_sieve_exact(SieveArgs a) {
+__global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
     constexpr int NW = THREADS / 32;
     constexpr uint64_t SEG = (uint64_t)TILE * NT;
     extern __shared__ __align__(16) unsigned long long sm64[];
-    unsigned long long* r = sm64;                        // TILE
+    unsigned long long* r = sm64;                        // TILE slots
     unsigned long long* bent = r + TILE;                 // NT * BCAP : (prog index << 16 | loc)
     unsigned long long* s_inv = bent + NT * BCAP;        // MAXS
     uint32_t* bcnt = (uint32_t*)(s_inv + MAXS);          // NT
-    uint32_t* s_q = bcnt + NT;                           // MAXS
+    uint32_t* s_q = bcnt + NT;                           // MAXS (sorted by q on the host)
     uint32_t* s_tm = s_q + MAXS;
     uint32_t* s_off = s_tm + MAXS;
-    uint32_t* s_two = s_off + MAXS;
+    uint32_t* s_item = s_off + MAXS;                     // 2 * MAXS work items
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nsmall = a.nsmall;
+    const int nsmall = a.nsmall, nitems = a.nitems;
     for (int j = tid; j < nsmall; j += THREADS) {
         const uint32_t q = (uint32_t)a.small[j].q, p = a.small[j].p;
         s_q[j] = q;
         s_tm[j] = (uint32_t)TILE % q;
-        s_two[j] = (p == 2);
-        s_inv[j] = (p == 2) ? 0ull : bnx_inv64(p);
+        s_inv[j] = (p == 2) ? 0ull : bnx_inv64(p);  // 0 marks p = 2: a right shift
     }
+    for (int j = tid; j < nitems; j += THREADS) s_item[j] = a.items[j];
     const uint64_t nseg = (a.length + SEG - 1) / SEG;
     for (uint64_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
         const uint64_t seg_off = seg * SEG;
@@ -534,29 +534,46 @@ __global__ void __launch_bounds__(THREADS) k_sieve_exact(SieveArgs a) {
             const uint64_t toff = seg_off + (uint64_t)t * TILE;
             if (toff >= a.length) break;
             const uint64_t tile0 = a.start + toff;
-            for (int i = tid; i < TILE; i += THREADS) {
-                const uint64_t x = tile0 + (uint64_t)i;
-                uint64_t v = x;
-                if (a.fast && x) {
-                    const int tz = bnx_ctz64(x);
-                    if (tz >= 2) v = x >> (tz - 1);
+            // init: x, or x with all but one factor two removed (_kernels.py:33-45); two
+            // integers per thread and 16-byte stores: exactly one of them is even, and only
+            // that one can need the shift.
+            for (int g = tid; g < TILE / 2; g += THREADS) {
+                const uint64_t x0 = tile0 + 2u * (uint32_t)g;
+                uint64_t v0 = x0, v1 = x0 + 1;
+                if (a.fast) {
+                    const bool odd0 = x0 & 1;
+                    const uint64_t xe = odd0 ? v1 : v0;
+                    if ((xe & 3) == 0 && xe) {
+                        const uint32_t lo = (uint32_t)xe;
+                        const int tz = lo ? __ffs(lo) - 1 : 31 + __ffs((uint32_t)(xe >> 32));
+                        const uint64_t ve = xe >> (tz - 1);
+                        if (odd0) v1 = ve; else v0 = ve;
+                    }
                 }
-                r[i] = v;
+                reinterpret_cast<ulonglong2*>(r)[g] = make_ulonglong2(v0, v1);
             }
             __syncthreads();
-            for (int j = 0; j < nsmall; ++j) {
-                const uint32_t q = s_q[j];
-                if (q >= 64) continue;
-                const uint64_t inv = s_inv[j];
-                const bool two = s_two[j];
-                for (uint32_t o = s_off[j] + tid * q; o < TILE; o += THREADS * q) div_slot(&r[o], inv, two);
-            }
-            for (int j = warp; j < nsmall; j += NW) {
-                const uint32_t q = s_q[j];
-                if (q < 64) continue;
-                const uint64_t inv = s_inv[j];
-                const bool two = s_two[j];
-                for (uint32_t o = s_off[j] + lane * q; o < TILE; o += 32 * q) div_slot(&r[o], inv, two);
+            // per-tile progressions: balanced work items (see k_screen), exact division per hit
+            for (int round = 0;; ++round) {
+                const int it = round * NW + ((round & 1) ? NW - 1 - warp : warp);
+                if (it >= nitems) break;
+                const uint32_t e = s_item[it];
+                const int j = (int)(e & 0xFFu);
+                if (e >> 31) {
+                    const int jj = j + lane;
+                    if (jj < nsmall) {
+                        const uint32_t q = s_q[jj];
+                        const uint64_t inv = s_inv[jj];
+                        for (uint32_t o = s_off[jj]; o < TILE; o += q) div_slot(&r[o], inv, inv == 0);
+                    }
+                } else {
+                    const uint32_t rr = (e >> 8) & 0xFFu, R = (e >> 16) & 0x7FFFu;
+                    const uint32_t q = s_q[j];
+                    const uint64_t inv = s_inv[j];
+                    const uint32_t step = 32u * R * q;
+                    for (uint32_t o = s_off[j] + (rr * 32u + (uint32_t)lane) * q; o < TILE; o += step)
+                        div_slot(&r[o], inv, inv == 0);
+                }
             }
             {
                 const uint32_t nb = min(bcnt[t], (uint32_t)BCAP);
@@ -572,12 +589,13 @@ __global__ void __launch_bounds__(THREADS) k_sieve_exact(SieveArgs a) {
                 if (no < 0) no += (int)s_q[j];
                 s_off[j] = (uint32_t)no;
             }
+            // write out: 16-byte streaming stores (the values are not re-read on the device)
             const uint64_t rem = a.length - toff;
             const int lim = rem < (uint64_t)TILE ? (int)rem : TILE;
             uint64_t* dst = a.out + toff;
             if (lim == TILE && ((((uintptr_t)dst) & 15) == 0)) {
                 for (int i = tid; i < TILE / 2; i += THREADS)
-                    reinterpret_cast<ulonglong2*>(dst)[i] = make_ulonglong2(r[2 * i], r[2 * i + 1]);
+                    __stcs(reinterpret_cast<ulonglong2*>(dst) + i, make_ulonglong2(r[2 * i], r[2 * i + 1]));
             } else {
                 for (int i = tid; i < lim; i += THREADS) dst[i] = r[i];
             }
@@ -645,7 +663,7 @@ __global__ void __launch_bounds__(256) k_brute_force(const uint64_t* __restrict_
 // Launch helpers (instantiations and dynamic shared memory sizes).
 size_t sieve_smem_bytes() {
     return sizeof(unsigned long long) * ((size_t)SIEVE_TILE + (size_t)SIEVE_NT * SIEVE_BCAP + SIEVE_MAXS) +
-           sizeof(uint32_t) * ((size_t)SIEVE_NT + 4 * SIEVE_MAXS);
+           sizeof(uint32_t) * ((size_t)SIEVE_NT + 5 * SIEVE_MAXS);
 }
 
 const void* sieve_kernel() {

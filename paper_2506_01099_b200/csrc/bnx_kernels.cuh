@@ -11,10 +11,10 @@ namespace bnx {
 // Screen: per-tile progressions (q < tile) at most SCREEN_MAXS; geometry variants below.
 constexpr int SCREEN_MAXS = 160;
 
-// Exact radical sieve geometry: 4096 u64 slots per tile (32 KB).
-constexpr int SIEVE_TILE = 4096;
+// Exact radical sieve geometry: 8192 u64 slots per tile (64 KB), 64 tiles per segment.
+constexpr int SIEVE_TILE = 8192;
 constexpr int SIEVE_NT = 64;
-constexpr int SIEVE_THREADS = 256;
+constexpr int SIEVE_THREADS = 512;
 constexpr int SIEVE_BCAP = 64;
 constexpr int SIEVE_MAXS = 160;
 
@@ -55,6 +55,8 @@ struct SieveArgs {
     int nsmall;
     const BnxProg* large;
     uint64_t nlarge;
+    const uint32_t* items;
+    int nitems;
     int fast;
     uint64_t* out;
     int* flags;
