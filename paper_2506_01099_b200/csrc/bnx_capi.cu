@@ -350,6 +350,7 @@ int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint6
     const uint64_t need = isqrt_u64(max_x);
     TRY(ensure_primes(c, primes, np, plimit, need));
     TRY(build_tables(c, c->screen_tab, max_x, 0, (uint32_t)screen_variant(c->screen_v).tile));
+    if (c->screen_tab.nitems > SCREEN_MAX_ITEMS) return fail(BNX_ERR_CUDA, "too many screen work items");
     if (c->screen_tab.nsmall > (uint32_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     return BNX_OK;
 }

@@ -20,7 +20,7 @@ for k in range(13):
 print(sum(ts) / len(ts))
 ''' % ROOT
 variant = os.environ.get("BNX_SCREEN_VARIANT", "1")
-for skip in [0, 1, 2, 4, 8, 16, 1 | 2, 1 | 2 | 4, 1 | 2 | 4 | 8, 31]:
+for skip in [int(x) for x in os.environ.get('SKIPS', '0,1,2,4,16,3,7,15,31').split(',')]:
     env = dict(os.environ, BNX_SCREEN_SKIP=str(skip), BNX_SCREEN_VARIANT=variant)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print(json.dumps({"variant": variant, "skip": skip, "screen_ms": out.stdout.strip(), "err": out.stderr[-300:] if out.returncode else ""}), flush=True)
