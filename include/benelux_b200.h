@@ -16,6 +16,8 @@
  *   bnx_search_domain           <- chunked.py:307-359        search_chunk(index, s, primes, n_limit)
  *                                  (+ chunked.py:362-412      run_full_chunked, one call per chunk)
  *   bnx_brute_force             <- bruteforce.py:16-42       brute_force_pairs(limit) (_kernels.py:235-263)
+ *   bnx_table_*                 <- chunked.py:129-359 +      SignatureTable / build_table / probe_table /
+ *                                  _kernels.py:130-232         search_chunk (the paper's Algorithm 3)
  *   bnx_slot_of                 <- _kernels.py:115-123 /     _slot_of / commutative_hash
  *                                  chunked.py:93-109
  *   status codes                <- _kernels.py:17-19         STATUS_OK / TABLE_FULL / BUFFER_FULL
@@ -139,6 +141,28 @@ BNX_API int bnx_prepare(bnx_ctx_t* ctx, uint64_t max_x, const uint64_t* primes, 
                 uint64_t primes_limit);
 BNX_API int bnx_search_enqueue(bnx_ctx_t* ctx, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask);
 BNX_API int bnx_search_collect(bnx_ctx_t* ctx, bnx_pair_t* out, size_t cap, size_t* found);
+
+/* ---- Algorithm 3 of the paper (chunked.py:129-359, _kernels.py:130-232) on the GPU -------
+ * An open-addressing signature table with the reference's slot word ((t+1) << 32 | home,
+ * 0 = empty), hash and linear probing, built by all threads at once (64-bit CAS).  The pair
+ * set equals the serial build's; slot placement may differ.  Rows sorted by (n, m).
+ * BNX_TABLE_FULL when a walk wraps the table (TableFullError). */
+typedef struct bnx_table bnx_table_t;
+BNX_API int bnx_table_create(bnx_ctx_t* ctx, uint64_t table_size, bnx_table_t** out);
+BNX_API int bnx_table_destroy(bnx_table_t* table);
+/* chunked.py:243-272 insert_all: domain elements t < count, n = domain_start + t < n_limit. */
+BNX_API int bnx_table_insert_all(bnx_table_t* table, uint64_t domain_start, const uint64_t* rad_of,
+                                 const uint64_t* rad_next, size_t count, uint64_t n_limit, bnx_pair_t* out,
+                                 size_t cap, size_t* found, uint64_t* inserted);
+/* chunked.py:274-304 probe_all: read-only probe with the domain starting at probe_start. */
+BNX_API int bnx_table_probe_all(bnx_table_t* table, uint64_t probe_start, const uint64_t* rad_of,
+                                const uint64_t* rad_next, size_t count, bnx_pair_t* out, size_t cap, size_t* found);
+/* copy of the slot words (table_size u64). */
+BNX_API int bnx_table_slots(const bnx_table_t* table, uint64_t* out, size_t cap);
+/* chunked.py:307-359 search_chunk with Algorithm 3 on the device: sieve chunk `index`, build
+ * its table, re-sieve and probe every earlier chunk j in [j_lo, j_hi). */
+BNX_API int bnx_table_search_chunk(bnx_ctx_t* ctx, uint64_t index, uint64_t chunk_size, uint64_t n_limit,
+                                   uint64_t j_lo, uint64_t j_hi, bnx_pair_t* out, size_t cap, size_t* found);
 
 /* _kernels.py:115-123: the reference's commutative slot hash (host, for API parity). */
 BNX_API uint64_t bnx_slot_of(uint64_t lo, uint64_t hi, uint64_t mask, uint64_t phi, uint64_t mul1, uint64_t mul2);

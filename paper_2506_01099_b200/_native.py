@@ -31,6 +31,8 @@ EXPORTED_SYMBOLS = (
     "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_primes_up_to", "bnx_sieve_radicals",
     "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain",
     "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of", "bnx_brute_force",
+    "bnx_table_create", "bnx_table_destroy", "bnx_table_insert_all", "bnx_table_probe_all", "bnx_table_slots",
+    "bnx_table_search_chunk",
 )
 
 
@@ -121,6 +123,17 @@ def load() -> ctypes.CDLL:
         L.bnx_search_domain.argtypes = [vp, ctypes.c_uint64] + search_args[1:]
         L.bnx_brute_force.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(PairRow), ctypes.c_size_t,
                                       ctypes.POINTER(ctypes.c_size_t)]
+        L.bnx_table_create.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
+        L.bnx_table_destroy.argtypes = [vp]
+        L.bnx_table_insert_all.argtypes = [vp, ctypes.c_uint64, _u64p, _u64p, ctypes.c_size_t, ctypes.c_uint64,
+                                           ctypes.POINTER(PairRow), ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
+                                           ctypes.POINTER(ctypes.c_uint64)]
+        L.bnx_table_probe_all.argtypes = [vp, ctypes.c_uint64, _u64p, _u64p, ctypes.c_size_t,
+                                          ctypes.POINTER(PairRow), ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+        L.bnx_table_slots.argtypes = [vp, _u64p, ctypes.c_size_t]
+        L.bnx_table_search_chunk.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.POINTER(PairRow), ctypes.c_size_t,
+                                             ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_prepare.argtypes = [vp, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_uint64]
         L.bnx_search_enqueue.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32]
         L.bnx_search_collect.argtypes = [vp, ctypes.POINTER(PairRow), ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]

@@ -142,6 +142,17 @@ struct bnx_ctx {
     bnx_stats_t stats{};
 };
 
+struct bnx_table {
+    bnx_ctx* ctx = nullptr;
+    uint64_t size = 0;
+    DBuf<uint64_t> slots;
+    DBuf<uint64_t> rad_of, rad_next, probe_of, probe_next;  // device copies of the domains
+    uint64_t domain_start = 0, count = 0;
+    DBuf<bnx_pair_t> rows;
+    DBuf<unsigned long long> cnt;  // [0] pairs [1] inserted
+    DBuf<int> status;
+};
+
 namespace {
 
 int activate(bnx_ctx* c) {
@@ -245,7 +256,8 @@ std::vector<uint32_t> build_items(const std::vector<BnxProg>& small, uint32_t ti
 }
 
 int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_t tile) {
-    if (t.gen == c->gen && t.max_x == max_x && t.include_two == include_two && t.tile == tile) return BNX_OK;
+    // a table built for a larger bound serves a smaller one: progressions q > x never divide x
+    if (t.gen == c->gen && t.max_x >= max_x && t.include_two == include_two && t.tile == tile) return BNX_OK;
     const uint64_t root = isqrt_u64(max_x);
     const uint64_t np = (uint64_t)(std::upper_bound(c->h_primes.begin(), c->h_primes.end(), (uint32_t)std::min<uint64_t>(root, 0xFFFFFFFFull)) - c->h_primes.begin());
     const uint64_t cb = icbrt_u64(max_x);
@@ -646,7 +658,7 @@ int bnx_prepare(bnx_ctx_t* c, uint64_t max_x, const uint64_t* primes, size_t npr
 int bnx_search_enqueue(bnx_ctx_t* c, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");
     if (n_first < 1 || n_last < n_first) return fail(BNX_ERR_INVALID, "empty search domain");
-    if (c->screen_tab.gen != c->gen || c->screen_tab.max_x < n_last + 1)
+    if (c->screen_tab.gen != c->gen || c->screen_tab.max_x < n_last + 1)  // prepared for a large enough bound
         return fail(BNX_ERR_INVALID, "bnx_prepare must cover n_last + 1 first");
     TRY(activate(c));
     return enqueue(c, n_first, n_last, kinds_mask & 3u);
@@ -683,6 +695,168 @@ int bnx_search_domain(bnx_ctx_t* c, uint64_t n_first, uint64_t n_last, uint32_t 
     std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
         return a.n != b.n ? a.n < b.n : a.m < b.m;
     });
+    return emit(rows, out, cap, found);
+}
+
+// ---- Algorithm 3 ----------------------------------------------------------------------
+static int table_run(bnx_table* tb, bool insert, uint64_t a0, uint64_t count, uint64_t n_limit,
+                     std::vector<bnx_pair_t>& rows, uint64_t* inserted) {
+    bnx_ctx* c = tb->ctx;
+    uint64_t cap = std::max<uint64_t>(tb->rows.cap, 1024);
+    for (;;) {
+        TRY(tb->rows.ensure(cap));
+        TRY(tb->cnt.ensure(2));
+        TRY(tb->status.ensure(1));
+        CK(cudaMemsetAsync(tb->cnt.p, 0, 2 * sizeof(unsigned long long), c->stream));
+        CK(cudaMemsetAsync(tb->status.p, 0, sizeof(int), c->stream));
+        if (insert) CK(cudaMemsetAsync(tb->slots.p, 0, sizeof(uint64_t) * tb->size, c->stream));
+        TableArgs ta{};
+        ta.domain_start = tb->domain_start;
+        ta.rad_of = tb->rad_of.p;
+        ta.rad_next = tb->rad_next.p;
+        ta.count_n = insert ? count : tb->count;
+        ta.n_limit = n_limit;
+        ta.probe_start = a0;
+        ta.probe_of = tb->probe_of.p;
+        ta.probe_next = tb->probe_next.p;
+        ta.count_m = insert ? 0 : count;
+        ta.slots = tb->slots.p;
+        ta.mask = tb->size - 1;
+        ta.out = tb->rows.p;
+        ta.cap = tb->rows.cap;
+        ta.count = tb->cnt.p;
+        ta.inserted = tb->cnt.p + 1;
+        ta.status = tb->status.p;
+        const int grid = c->num_sms * 8;
+        if (insert) launch_table_insert(ta, grid, c->stream);
+        else launch_table_probe(ta, grid, c->stream);
+        CK(cudaGetLastError());
+        unsigned long long h[2] = {0, 0};
+        int st = 0;
+        CK(cudaMemcpyAsync(h, tb->cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&st, tb->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (st == BNX_TABLE_FULL) return fail(BNX_TABLE_FULL, "no empty slot in a table of " + std::to_string(tb->size));
+        if (h[0] > tb->rows.cap) { cap = h[0] * 2; continue; }
+        const size_t base = rows.size();
+        rows.resize(base + h[0]);
+        if (h[0]) CK(cudaMemcpy(rows.data() + base, tb->rows.p, sizeof(bnx_pair_t) * h[0], cudaMemcpyDeviceToHost));
+        if (inserted) *inserted = h[1];
+        return BNX_OK;
+    }
+}
+
+static void sort_nm(std::vector<bnx_pair_t>& rows) {
+    std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
+        return a.n != b.n ? a.n < b.n : a.m < b.m;
+    });
+}
+
+int bnx_table_create(bnx_ctx_t* c, uint64_t table_size, bnx_table_t** out) {
+    if (!c || !out) return fail(BNX_ERR_INVALID, "null argument");
+    if (table_size < 1 || (table_size & (table_size - 1))) return fail(BNX_ERR_INVALID, "table size must be a power of two");
+    if (table_size > (1ull << 32)) return fail(BNX_ERR_INVALID, "table too large for 32-bit home slots");
+    TRY(activate(c));
+    bnx_table* tb = new bnx_table();
+    tb->ctx = c;
+    tb->size = table_size;
+    int r = tb->slots.ensure(table_size);
+    if (r != BNX_OK) { delete tb; return r; }
+    CK(cudaMemsetAsync(tb->slots.p, 0, sizeof(uint64_t) * table_size, c->stream));
+    *out = tb;
+    return BNX_OK;
+}
+
+int bnx_table_destroy(bnx_table_t* tb) {
+    if (!tb) return BNX_OK;
+    cudaSetDevice(tb->ctx->device);
+    cudaStreamSynchronize(tb->ctx->stream);
+    tb->slots.release(); tb->rad_of.release(); tb->rad_next.release();
+    tb->probe_of.release(); tb->probe_next.release(); tb->rows.release(); tb->cnt.release(); tb->status.release();
+    delete tb;
+    return BNX_OK;
+}
+
+int bnx_table_insert_all(bnx_table_t* tb, uint64_t domain_start, const uint64_t* rad_of, const uint64_t* rad_next,
+                         size_t count, uint64_t n_limit, bnx_pair_t* out, size_t cap, size_t* found, uint64_t* inserted) {
+    if (!tb) return fail(BNX_ERR_INVALID, "null table");
+    if (count > 0xFFFFFFFEull) return fail(BNX_ERR_INVALID, "domain too large for 32-bit slot offsets");
+    TRY(activate(tb->ctx));
+    TRY(tb->rad_of.ensure(count));
+    TRY(tb->rad_next.ensure(count));
+    if (count) {
+        CK(cudaMemcpyAsync(tb->rad_of.p, rad_of, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, tb->ctx->stream));
+        CK(cudaMemcpyAsync(tb->rad_next.p, rad_next, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, tb->ctx->stream));
+    }
+    tb->domain_start = domain_start;
+    tb->count = count;
+    std::vector<bnx_pair_t> rows;
+    TRY(table_run(tb, true, 0, count, n_limit, rows, inserted));
+    sort_nm(rows);
+    return emit(rows, out, cap, found);
+}
+
+int bnx_table_probe_all(bnx_table_t* tb, uint64_t probe_start, const uint64_t* rad_of, const uint64_t* rad_next,
+                        size_t count, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (!tb) return fail(BNX_ERR_INVALID, "null table");
+    TRY(activate(tb->ctx));
+    TRY(tb->probe_of.ensure(count));
+    TRY(tb->probe_next.ensure(count));
+    if (count) {
+        CK(cudaMemcpyAsync(tb->probe_of.p, rad_of, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, tb->ctx->stream));
+        CK(cudaMemcpyAsync(tb->probe_next.p, rad_next, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, tb->ctx->stream));
+    }
+    std::vector<bnx_pair_t> rows;
+    TRY(table_run(tb, false, probe_start, count, 0, rows, nullptr));
+    std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
+        return a.m != b.m ? a.m < b.m : a.n < b.n;
+    });
+    return emit(rows, out, cap, found);
+}
+
+int bnx_table_slots(const bnx_table_t* tb, uint64_t* out, size_t cap) {
+    if (!tb || !out) return fail(BNX_ERR_INVALID, "null argument");
+    if (cap < tb->size) return fail(BNX_BUFFER_FULL, "slot buffer too small");
+    CK(cudaSetDevice(tb->ctx->device));
+    CK(cudaStreamSynchronize(tb->ctx->stream));
+    CK(cudaMemcpy(out, tb->slots.p, sizeof(uint64_t) * tb->size, cudaMemcpyDeviceToHost));
+    return BNX_OK;
+}
+
+int bnx_table_search_chunk(bnx_ctx_t* c, uint64_t index, uint64_t chunk_size, uint64_t n_limit, uint64_t j_lo,
+                           uint64_t j_hi, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (chunk_size < 3) return fail(BNX_ERR_INVALID, "chunk size must be >= 3");
+    TRY(activate(c));
+    const uint64_t s = chunk_size, count = s - 1;
+    uint64_t v = 4 * count - 1, bits = 0;
+    while (v) { ++bits; v >>= 1; }
+    const uint64_t tsize = 1ull << bits;  // table_size_for (chunked.py:86-90)
+    bnx_table tb;
+    tb.ctx = c;
+    tb.size = tsize;
+    TRY(tb.slots.ensure(tsize));
+    TRY(tb.rad_of.ensure(s));
+    TRY(tb.probe_of.ensure(s));
+    const uint64_t first = 1 + index * (s - 1);
+    std::vector<bnx_pair_t> rows;
+    TRY(sieve_common(c, first, s, nullptr, 0, 0, 1, nullptr, tb.rad_of.p));
+    tb.rad_next.p = tb.rad_of.p + 1;  // views, as chunked.py:330-332
+    tb.domain_start = first;
+    tb.count = count;
+    int r = table_run(&tb, true, 0, count, n_limit, rows, nullptr);
+    for (uint64_t j = j_lo; r == BNX_OK && j < j_hi; ++j) {
+        const uint64_t fj = 1 + j * (s - 1);
+        r = sieve_common(c, fj, s, nullptr, 0, 0, 1, nullptr, tb.probe_of.p);
+        if (r != BNX_OK) break;
+        tb.probe_next.p = tb.probe_of.p + 1;
+        r = table_run(&tb, false, fj, count, 0, rows, nullptr);
+    }
+    tb.rad_next.p = nullptr;
+    tb.probe_next.p = nullptr;
+    tb.slots.release(); tb.rad_of.release(); tb.probe_of.release(); tb.rows.release(); tb.cnt.release(); tb.status.release();
+    TRY(r);
+    sort_nm(rows);
     return emit(rows, out, cap, found);
 }
 

@@ -660,6 +660,76 @@ __global__ void __launch_bounds__(256) k_brute_force(const uint64_t* __restrict_
 }
 
 // ------------------------------------------------------------------------------------
+// Algorithm 3 of the paper on the GPU (chunked.py:129-304, _kernels.py:115-232): the
+// open-addressing signature table with the reference's slot word ((t+1) << 32 | home, 0 =
+// empty), hash (_slot_of) and linear probing, built by all threads at once with 64-bit
+// CAS.  Two elements with equal signatures share a home slot, and whichever claims its
+// slot later walks past the earlier one, so every equal pair is reported exactly once (as
+// (smaller, larger) domain index, classified like _kernels.py:172).  Slot placement can
+// differ from the serial build; the pair set cannot.
+__device__ __forceinline__ uint64_t table_slot_of(uint64_t lo, uint64_t hi, uint64_t mask) {
+    uint64_t x = lo ^ (hi * 0x9E3779B97F4A7C15ull);
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return (x ^ (x >> 31)) & mask;
+}
+
+__device__ __forceinline__ void table_emit(TableArgs& a, int kind, uint64_t m, uint64_t n, uint64_t rm, uint64_t rm1) {
+    unsigned long long k = atomicAdd(a.count, 1ull);
+    if (k < a.cap) a.out[k] = bnx_pair_t{m, n, rm, rm1, kind, 0};
+}
+
+__global__ void k_table_insert(TableArgs a) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < a.count_n; t += (uint64_t)gridDim.x * blockDim.x) {
+        if (a.domain_start + t >= a.n_limit) continue;
+        const uint64_t x = a.rad_of[t], y = a.rad_next[t];
+        const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
+        const uint64_t home = table_slot_of(lo, hi, a.mask);
+        const unsigned long long mine = ((unsigned long long)(t + 1) << 32) | home;
+        uint64_t idx = home, steps = 0;
+        for (;;) {
+            unsigned long long stored = a.slots[idx];
+            if (stored == 0) {
+                stored = atomicCAS(reinterpret_cast<unsigned long long*>(a.slots) + idx, 0ull, mine);
+                if (stored == 0) { atomicAdd(a.inserted, 1ull); break; }
+            }
+            if ((stored & 0xFFFFFFFFull) == home) {
+                const uint64_t tp = (stored >> 32) - 1;
+                const uint64_t x2 = a.rad_of[tp], y2 = a.rad_next[tp];
+                if ((x2 < y2 ? x2 : y2) == lo && (x2 < y2 ? y2 : x2) == hi) {
+                    const uint64_t tm = tp < t ? tp : t, tn = tp < t ? t : tp;
+                    const uint64_t rm = a.rad_of[tm], rm1 = a.rad_next[tm];
+                    table_emit(a, rm == a.rad_of[tn] ? 1 : 2, a.domain_start + tm, a.domain_start + tn, rm, rm1);
+                }
+            }
+            idx = (idx + 1) & a.mask;
+            if (++steps > a.mask) { *a.status = BNX_TABLE_FULL; break; }
+        }
+    }
+}
+
+__global__ void k_table_probe(TableArgs a) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < a.count_m; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = a.probe_of[t], y = a.probe_next[t];
+        const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
+        const uint64_t home = table_slot_of(lo, hi, a.mask);
+        uint64_t idx = home, steps = 0;
+        for (;;) {
+            const uint64_t stored = a.slots[idx];
+            if (stored == 0) break;
+            if ((stored & 0xFFFFFFFFull) == home) {
+                const uint64_t tp = (stored >> 32) - 1;
+                const uint64_t x2 = a.rad_of[tp], y2 = a.rad_next[tp];
+                if ((x2 < y2 ? x2 : y2) == lo && (x2 < y2 ? y2 : x2) == hi)
+                    table_emit(a, x == x2 ? 1 : 2, a.probe_start + t, a.domain_start + tp, x, y);
+            }
+            idx = (idx + 1) & a.mask;
+            if (++steps > a.mask) { *a.status = BNX_TABLE_FULL; break; }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
 size_t sieve_smem_bytes() {
     return sizeof(unsigned long long) * ((size_t)SIEVE_TILE + (size_t)SIEVE_NT * SIEVE_BCAP + SIEVE_MAXS) +
@@ -728,6 +798,8 @@ void launch_brute_force(const uint64_t* rads, uint64_t limit, bnx_pair_t* out, u
     const uint64_t blocks = (limit + 255) / 256;
     k_brute_force<<<(unsigned)blocks, 256, 0, st>>>(rads, limit, out, cap, count);
 }
+void launch_table_insert(const TableArgs& a, int grid, cudaStream_t st) { k_table_insert<<<grid, 256, 0, st>>>(a); }
+void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st) { k_table_probe<<<grid, 256, 0, st>>>(a); }
 void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out,
                            int grid, cudaStream_t st) {
     k_trial_division<<<grid, 256, 0, st>>>(start, length, pd, npd, out);

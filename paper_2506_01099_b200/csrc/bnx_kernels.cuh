@@ -73,6 +73,27 @@ struct ScreenVariant {
 };
 int screen_variant_count();
 const ScreenVariant& screen_variant(int i);
+// Algorithm 3 (signature table) arguments.
+struct TableArgs {
+    uint64_t domain_start;
+    const uint64_t* rad_of;     // table chunk: rad(domain_start + t), t < count_n
+    const uint64_t* rad_next;   // rad(domain_start + t + 1)
+    uint64_t count_n;
+    uint64_t n_limit;           // insert only n < n_limit
+    uint64_t probe_start;
+    const uint64_t* probe_of;   // probing chunk
+    const uint64_t* probe_next;
+    uint64_t count_m;
+    uint64_t* slots;
+    uint64_t mask;
+    bnx_pair_t* out;
+    uint64_t cap;
+    unsigned long long* count;
+    unsigned long long* inserted;
+    int* status;
+};
+void launch_table_insert(const TableArgs& a, int grid, cudaStream_t st);
+void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st);
 size_t sieve_smem_bytes();
 const void* sieve_kernel();
 void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st);
