@@ -1,0 +1,95 @@
+"""Raw C ABI on the GPU: the status-code protocol (_kernels.py:17-19 semantics), the
+split-phase API, stream attachment and the device-memory sieve."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+_native = pytest.importorskip("paper_2506_01099_b200._native")
+
+
+@pytest.fixture(scope="module")
+def L():
+    return _native.load()
+
+
+@pytest.fixture(scope="module")
+def ctx(L):
+    h = ctypes.c_void_p()
+    assert L.bnx_ctx_create(0, ctypes.byref(h)) == _native.BNX_OK
+    yield h
+    L.bnx_ctx_destroy(h)
+
+
+def test_buffer_full_protocol(L, ctx, golden):
+    found = ctypes.c_size_t(0)
+    small = (_native.PairRow * 4)()
+    st = L.bnx_search(ctx, 2**32, 3, None, 0, 0, small, 4, ctypes.byref(found))
+    assert st == _native.BNX_BUFFER_FULL and found.value == 33
+    big = (_native.PairRow * found.value)()
+    assert L.bnx_search(ctx, 2**32, 3, None, 0, 0, big, found.value, ctypes.byref(found)) == _native.BNX_OK
+    rows = [[r.kind, r.m, r.n, r.rad_m, r.rad_m1] for r in big]
+    exp = golden["expected_pairs_up_to"]["4294967296"]
+    assert rows == sorted(exp["first"] + exp["second"], key=lambda r: (r[1], r[2]))
+
+
+def test_error_codes(L, ctx):
+    found = ctypes.c_size_t(0)
+    buf = (_native.PairRow * 4)()
+    assert L.bnx_search(ctx, 2, 3, None, 0, 0, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_INVALID
+    assert L.bnx_search(ctx, 100, 0, None, 0, 0, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_INVALID
+    assert L.bnx_search(ctx, 1 << 43, 3, None, 0, 0, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_RANGE
+    primes = np.array([2, 3, 5, 7], np.uint64)
+    p = primes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    assert L.bnx_search(ctx, 10**6, 3, p, 4, 10, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_PRIMES_UNCOVERED
+    assert b"covers" in L.bnx_last_error()
+    out = np.empty(10, np.uint64)
+    assert L.bnx_sieve_radicals(ctx, 0, 10, None, 0, 0, 1, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))) \
+        == _native.BNX_ERR_INVALID
+
+
+def test_split_phase_and_stats():
+    ctx = _native.Context(0)
+    try:
+        ctx.set_timing(True)
+        ctx.prepare(2**32)
+        ctx.enqueue(1, 2**32 - 1, 1)
+        rows = ctx.collect()
+        assert len(rows) == 16 and all(int(k) == 1 for k in rows["kind"])
+        st = ctx.stats()
+        assert st["integers"] == 2**32 - 1 and st["pairs"] == 16 and st["candidates"] >= 16
+        screen_ms, pipe_ms = ctx.timing()
+        assert 0 < screen_ms <= pipe_ms
+        with pytest.raises(ValueError):
+            ctx.enqueue(1, 2**33, 1)  # not prepared that far
+    finally:
+        ctx.close()
+
+
+def test_torch_stream_and_device_sieve():
+    torch = pytest.importorskip("torch")
+    ctx = _native.Context(0)
+    try:
+        s = torch.cuda.Stream()
+        ctx.set_stream(s.cuda_stream)
+        out = torch.empty(1 << 20, dtype=torch.int64, device="cuda")
+        with torch.cuda.stream(s):
+            ctx.sieve_radicals_dev(1, out.numel(), out.data_ptr())
+        s.synchronize()
+        from oracle import oracle as orc
+
+        want = orc.sieve_segment(1, 1 << 20, orc.primes_up_to(1024))
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want)
+    finally:
+        ctx.close()
+
+
+def test_domain_search_equals_filtered_full(L, ctx):
+    found = ctypes.c_size_t(0)
+    buf = (_native.PairRow * 64)()
+    assert L.bnx_search_domain(ctx, 1000, 5_000_000, 3, None, 0, 0, buf, 64, ctypes.byref(found)) == 0
+    dom = [(r.m, r.n) for r in buf[: found.value]]
+    assert L.bnx_search(ctx, 5_000_001, 3, None, 0, 0, buf, 64, ctypes.byref(found)) == 0
+    full = sorted(((r.m, r.n) for r in buf[: found.value] if r.n >= 1000), key=lambda x: (x[1], x[0]))
+    assert dom == full
