@@ -237,25 +237,42 @@ int ensure_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
 
 // Work items of the screen's per-tile progressions (q < tile, sorted by q): a progression
 // with q < 2048 is split into R interleaved items of about ITEM_HITS hits per tile; the
-// rest go 32 progressions per item (one per lane).  Items are ordered by decreasing hits so
-// the snake deal in k_screen balances the warps.  Encoding: j | r << 8 | R << 16 | packed << 31.
-std::vector<uint32_t> build_items(const std::vector<BnxProg>& small, uint32_t tile) {
+// rest go 32 progressions per item (one per lane).  Encoding: j | r << 8 | R << 16 |
+// packed << 31.  The items are dealt to the `nwarps` warps of a CTA by longest-processing-
+// time-first on a cost model (SASS-measured: ~40 instructions of setup per item, ~4 per
+// split-loop iteration, ~9 per lane-packed iteration), so the warps reach the tile barrier
+// together.  Layout returned: [nwarps + 1 offsets][items grouped by warp].
+std::vector<uint32_t> build_items(const std::vector<BnxProg>& small, uint32_t tile, int nwarps) {
     constexpr uint32_t ITEM_HITS = 32 * 12;
+    constexpr uint32_t C_SETUP = 40, C_SPLIT = 4, C_PACKED = 9;
     std::vector<std::pair<uint32_t, uint32_t>> v;  // (cost, item)
     size_t j = 0;
     for (; j < small.size() && small[j].q < 2048; ++j) {
         const uint32_t hits = tile / (uint32_t)small[j].q;
         const uint32_t R = std::max(1u, (hits + ITEM_HITS / 2) / ITEM_HITS);
-        for (uint32_t r = 0; r < R; ++r) v.push_back({hits / R, (uint32_t)j | (r << 8) | (R << 16)});
+        const uint32_t iters = (hits / R + 31) / 32;
+        for (uint32_t r = 0; r < R; ++r) v.push_back({C_SETUP + C_SPLIT * iters, (uint32_t)j | (r << 8) | (R << 16)});
     }
-    for (; j < small.size(); j += 32) v.push_back({tile / (uint32_t)small[j].q, (uint32_t)j | (1u << 31)});
+    for (; j < small.size(); j += 32)
+        v.push_back({C_SETUP + C_PACKED * ((tile + (uint32_t)small[j].q - 1) / (uint32_t)small[j].q),
+                     (uint32_t)j | (1u << 31)});
     std::stable_sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-    std::vector<uint32_t> out;
-    for (auto& e : v) out.push_back(e.second);
+    std::vector<std::vector<uint32_t>> per(nwarps);
+    std::vector<uint64_t> load(nwarps, 0);
+    for (auto& e : v) {
+        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[w] += e.first;
+        per[w].push_back(e.second);
+    }
+    std::vector<uint32_t> out(nwarps + 1, 0);
+    for (int w = 0; w < nwarps; ++w) {
+        out[w + 1] = out[w] + (uint32_t)per[w].size();
+    }
+    for (int w = 0; w < nwarps; ++w) out.insert(out.end(), per[w].begin(), per[w].end());
     return out;
 }
 
-int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_t tile) {
+int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_t tile, int nwarps) {
     // a table built for a larger bound serves a smaller one: progressions q > x never divide x
     if (t.gen == c->gen && t.max_x >= max_x && t.include_two == include_two && t.tile == tile) return BNX_OK;
     const uint64_t root = isqrt_u64(max_x);
@@ -298,7 +315,7 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
         std::sort(hs.begin(), hs.end(), [](const BnxProg& x, const BnxProg& y) { return x.q < y.q; });
         CK(cudaMemcpy(t.small.p, hs.data(), sizeof(BnxProg) * ns, cudaMemcpyHostToDevice));
     }
-    std::vector<uint32_t> items = build_items(hs, tile);
+    std::vector<uint32_t> items = build_items(hs, tile, nwarps);
     if (items.size() > 2 * (size_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many screen work items");
     TRY(t.items.ensure(items.size() + 1));
     if (!items.empty())
@@ -361,8 +378,9 @@ int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint6
     if (max_x >= (1ull << 42)) return fail(BNX_ERR_RANGE, "search bound must be below 2^42");
     const uint64_t need = isqrt_u64(max_x);
     TRY(ensure_primes(c, primes, np, plimit, need));
-    TRY(build_tables(c, c->screen_tab, max_x, 0, (uint32_t)screen_variant(c->screen_v).tile));
-    if (c->screen_tab.nitems > SCREEN_MAX_ITEMS) return fail(BNX_ERR_CUDA, "too many screen work items");
+    TRY(build_tables(c, c->screen_tab, max_x, 0, (uint32_t)screen_variant(c->screen_v).tile,
+                     screen_variant(c->screen_v).threads / 32));
+
     if (c->screen_tab.nsmall > (uint32_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     return BNX_OK;
 }
@@ -555,7 +573,7 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
     const uint64_t end = start + (length - 1);
     const uint64_t need = isqrt_u64(end);
     TRY(ensure_primes(c, primes, np, plimit, need));
-    TRY(build_tables(c, c->sieve_tab, end, fast ? 0 : 1, SIEVE_TILE));
+    TRY(build_tables(c, c->sieve_tab, end, fast ? 0 : 1, SIEVE_TILE, SIEVE_THREADS / 32));
     if (c->sieve_tab.nsmall > (uint32_t)SIEVE_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     TRY(c->flags.ensure(4));
     if (!c->h_flags) CK(cudaMallocHost(&c->h_flags, sizeof(int) * 4));
@@ -599,7 +617,7 @@ int bnx_radicals_trial_division(bnx_ctx_t* c, uint64_t start, uint64_t length, u
     TRY(activate(c));
     const uint64_t end = start + (length - 1);
     TRY(ensure_primes(c, nullptr, 0, 0, isqrt_u64(end)));
-    TRY(build_tables(c, c->td_tab, end, 0, SIEVE_TILE));
+    TRY(build_tables(c, c->td_tab, end, 0, SIEVE_TILE, SIEVE_THREADS / 32));
     const uint64_t piece = std::min<uint64_t>(length, 1ull << 26);
     TRY(c->sieve_out.ensure(piece));
     for (uint64_t off = 0; off < length; off += piece) {
@@ -619,7 +637,7 @@ int bnx_brute_force(bnx_ctx_t* c, uint64_t limit, bnx_pair_t* out, size_t cap, s
     if (limit > (1ull << 22)) return fail(BNX_ERR_RANGE, "brute force is limited to 2^22 (quadratic)");
     TRY(activate(c));
     TRY(ensure_primes(c, nullptr, 0, 0, isqrt_u64(limit)));
-    TRY(build_tables(c, c->td_tab, limit, 0, SIEVE_TILE));
+    TRY(build_tables(c, c->td_tab, limit, 0, SIEVE_TILE, SIEVE_THREADS / 32));
     DBuf<uint64_t> rads;
     DBuf<bnx_pair_t> rows;
     DBuf<unsigned long long> cnt;

@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
     }
     for (int j = tid; j < a.nitems; j += THREADS) s_item[j] = a.items[j];
     __syncthreads();
-    const int nitems = a.nitems;
     // 2-adic half-bits 2(v2(x) - 1) of x = tile0 + 4j for the first word of each of this
     // thread's groups (j = 4i, i = tid + k*THREADS): tile0 is a multiple of TILE > 4j, so
     // v2(x) = 2 + v2(j) and the value is 2*ffs(j), the same for every k unless tid == 0.
@@ -286,11 +285,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
             }
             __syncthreads();
             // ---- progressions q < TILE: balanced work items
-            for (int round = 0; !(a.skip & 1); ++round) {
-                // snake order over the size-sorted items
-                const int it = round * NW + ((round & 1) ? NW - 1 - warp : warp);
-                if (it >= nitems) break;
-                const uint32_t e = s_item[it];
+            const int it_end = (a.skip & 1) ? 0 : (int)s_item[warp + 1];
+            for (int it = (int)s_item[warp]; it < it_end; ++it) {  // this warp's items (host LPT deal)
+                const uint32_t e = s_item[NW + 1 + it];
                 const int j = (int)(e & 0xFFu);
                 if (e >> 31) {  // lane-packed: one progression per lane
                     const int jj = j + lane;
@@ -554,10 +551,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
             }
             __syncthreads();
             // per-tile progressions: balanced work items (see k_screen), exact division per hit
-            for (int round = 0;; ++round) {
-                const int it = round * NW + ((round & 1) ? NW - 1 - warp : warp);
-                if (it >= nitems) break;
-                const uint32_t e = s_item[it];
+            const int it_end = (int)s_item[warp + 1];
+            for (int it = (int)s_item[warp]; it < it_end; ++it) {
+                const uint32_t e = s_item[NW + 1 + it];
                 const int j = (int)(e & 0xFFu);
                 if (e >> 31) {
                     const int jj = j + lane;
@@ -754,12 +750,13 @@ void launch_screen_v(const ScreenArgs& a, int grid, cudaStream_t st) {
     ScreenVariant{T, N, H, B, (const void*)k_screen<T, N, H, B, SCREEN_MAXS, M>, screen_smem<T, N, H, B>(), \
                   launch_screen_v<T, N, H, B, M>}
 static const ScreenVariant kScreenVariants[] = {
+    BNX_SCREEN_VARIANT(65536, 16, 512, 224, 2),  // default: fastest measured (profiles/)
     BNX_SCREEN_VARIANT(32768, 32, 512, 128, 4),
     BNX_SCREEN_VARIANT(32768, 32, 512, 128, 3),
     BNX_SCREEN_VARIANT(32768, 32, 256, 128, 8),
     BNX_SCREEN_VARIANT(16384, 64, 256, 96, 8),
-    BNX_SCREEN_VARIANT(65536, 16, 512, 224, 2),
     BNX_SCREEN_VARIANT(16384, 64, 512, 96, 4),
+    BNX_SCREEN_VARIANT(65536, 16, 1024, 224, 2),
 };
 int screen_variant_count() { return (int)(sizeof(kScreenVariants) / sizeof(kScreenVariants[0])); }
 const ScreenVariant& screen_variant(int i) { return kScreenVariants[i]; }

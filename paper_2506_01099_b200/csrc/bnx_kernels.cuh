@@ -10,7 +10,6 @@ namespace bnx {
 
 // Screen: per-tile progressions (q < tile) at most SCREEN_MAXS; geometry variants below.
 constexpr int SCREEN_MAXS = 160;
-constexpr int SCREEN_MAX_ITEMS = 64;  // work items of the per-tile progressions (host-checked)
 
 // Exact radical sieve geometry: 8192 u64 slots per tile (64 KB), 64 tiles per segment.
 constexpr int SIEVE_TILE = 8192;
