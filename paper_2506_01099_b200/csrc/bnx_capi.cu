@@ -347,14 +347,13 @@ int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     Tables& t = c->screen_tab;
     TRY(ensure_work(c));
     const ScreenVariant& sv = screen_variant(c->screen_v);
-    const uint64_t SEG = (uint64_t)sv.tile * sv.nt;
     const uint64_t x_begin = n_first / sv.tile * sv.tile;
-    const uint64_t nseg = (n_last - x_begin + 1 + SEG - 1) / SEG;
+    const uint64_t ntiles = (n_last - x_begin) / sv.tile + 1;
     CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
-    ScreenArgs sa{x_begin, nseg, n_first, n_last, t.small.p, (int)t.nsmall, t.large.p, (int)t.nlarge,
+    ScreenArgs sa{x_begin, ntiles, n_first, n_last, t.small.p, (int)t.nsmall, t.large.p, (int)t.nlarge,
                   t.items.p, t.nitems, c->surv.p, c->surv.cap, c->ctr.p, c->flags.p, c->screen_skip};
-    const int sgrid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->screen_blocks_per_sm);
+    const int sgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)c->num_sms * c->screen_blocks_per_sm);
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     sv.launch(sa, sgrid, c->stream);
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));

@@ -204,7 +204,6 @@ __global__ void k_build_tables(const uint32_t* primes, uint64_t np, uint64_t max
 template <int TILE, int NT, int THREADS, int BCAP, int MAXS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
     constexpr int NW = THREADS / 32;
-    constexpr uint32_t SEG = (uint32_t)TILE * NT;
     constexpr int WORDS = TILE / 4;
     constexpr int GROUPS = WORDS / 4;  // 16 integers each
     constexpr int GPT = GROUPS / THREADS;
@@ -238,8 +237,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
     // v2(x) = 2 + v2(j) and the value is 2*ffs(j), the same for every k unless tid == 0.
     const uint32_t c_grp = 2u * (uint32_t)__ffs(4 * (tid ? tid : THREADS));
 
-    for (uint64_t seg = blockIdx.x; seg < a.nseg; seg += gridDim.x) {
-        const uint64_t seg0 = a.x_begin + seg * SEG;
+    // Each CTA owns an equal contiguous run of tiles (to within one), processed in segments of
+    // up to NT tiles: the grid finishes together whatever the bound.
+    const uint64_t t_begin = a.ntiles * blockIdx.x / gridDim.x, t_end = a.ntiles * (blockIdx.x + 1) / gridDim.x;
+    for (uint64_t st = t_begin; st < t_end; st += NT) {
+        const int nt = (int)min((uint64_t)NT, t_end - st);
+        const uint32_t seg_len = (uint32_t)nt * TILE;
+        const uint64_t seg0 = a.x_begin + st * TILE;
         __syncthreads();
         for (int j = tid; j < NT; j += THREADS) bcnt[j] = 0;
         for (int j = tid; j < nsmall; j += THREADS) {
@@ -252,10 +256,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
             const BnxProg pr = a.large[j];
             uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip);
             if (seg0 == 0 && o == 0) o = pr.q;
-            for (; o < SEG + 4; o += pr.q) {
+            for (; o < seg_len + 4; o += pr.q) {
                 const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
                 const uint32_t ent = pr.w << 17;  // loc needs 17 bits: TILE + 4 > 2^16
-                if (t < NT) {
+                if (t < (uint32_t)nt) {
                     uint32_t k = atomicAdd(&bcnt[t], 1u);
                     if (k < BCAP) bent[t * BCAP + k] = loc | ent; else a.flags[0] = 1;
                 }
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
         }
         __syncthreads();
 
-        for (int t = 0; t < NT; ++t) {
+        for (int t = 0; t < nt; ++t) {
             const uint64_t tile0 = seg0 + (uint64_t)t * TILE;
             if (tile0 > a.n_last) break;
             // ---- init with the 2-adic part
@@ -750,13 +754,10 @@ void launch_screen_v(const ScreenArgs& a, int grid, cudaStream_t st) {
     ScreenVariant{T, N, H, B, (const void*)k_screen<T, N, H, B, SCREEN_MAXS, M>, screen_smem<T, N, H, B>(), \
                   launch_screen_v<T, N, H, B, M>}
 static const ScreenVariant kScreenVariants[] = {
-    BNX_SCREEN_VARIANT(65536, 16, 512, 224, 2),  // default: fastest measured (profiles/)
+    BNX_SCREEN_VARIANT(65536, 64, 512, 128, 2),  // default: fastest measured (profiles/)
+    BNX_SCREEN_VARIANT(65536, 32, 512, 224, 2),
+    BNX_SCREEN_VARIANT(32768, 64, 512, 96, 3),
     BNX_SCREEN_VARIANT(32768, 32, 512, 128, 4),
-    BNX_SCREEN_VARIANT(32768, 32, 512, 128, 3),
-    BNX_SCREEN_VARIANT(32768, 32, 256, 128, 8),
-    BNX_SCREEN_VARIANT(16384, 64, 256, 96, 8),
-    BNX_SCREEN_VARIANT(16384, 64, 512, 96, 4),
-    BNX_SCREEN_VARIANT(65536, 16, 1024, 224, 2),
 };
 int screen_variant_count() { return (int)(sizeof(kScreenVariants) / sizeof(kScreenVariants[0])); }
 const ScreenVariant& screen_variant(int i) { return kScreenVariants[i]; }

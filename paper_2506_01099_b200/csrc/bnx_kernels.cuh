@@ -22,8 +22,8 @@ constexpr int SIEVE_MAXS = 160;
 constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_N = 8;
 
 struct ScreenArgs {
-    uint64_t x_begin;  // multiple of SCREEN_TILE
-    uint64_t nseg;
+    uint64_t x_begin;  // multiple of the tile
+    uint64_t ntiles;   // tiles covering [x_begin, n_last]
     uint64_t n_first, n_last;
     const BnxProg* small;
     int nsmall;
