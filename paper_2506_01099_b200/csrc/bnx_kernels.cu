@@ -331,27 +331,31 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
                 if (no < 0) no += (int)s_q[j];
                 s_off[j] = (uint32_t)no;
             }
-            // ---- scan
+            // ---- scan: pair sums of 16 integers, exact SWAR byte compare against the tile
+            // threshold (A(x) <= 108, so no byte carries); a divergent branch only on a hit
             const bool low = tile0 < (1u << 20);
-            const int tt = max(0, bnx_floor2log2(tile0 + 1) - 2);
-            const uint32_t pre = tt >= 2 ? ((0xFFu << (31 - __clz(tt))) & 0xFFu) * 0x01010101u : 0xFFFFFFFFu;
+            const uint32_t tt = (uint32_t)max(0, bnx_floor2log2(tile0 + 1) - 2);
 #pragma unroll
             for (int k = 0; k < ((a.skip & 4) ? 0 : GPT); ++k) {
                 const int i = tid + k * THREADS;
                 const uint4 v = reinterpret_cast<const uint4*>(acc)[i];
-                const uint32_t nx = acc[4 * i + 4];
-                const uint32_t s0 = v.x + __funnelshift_r(v.x, v.y, 8);  // A(x) + A(x+1), 4 bytes
-                const uint32_t s1 = v.y + __funnelshift_r(v.y, v.z, 8);
-                const uint32_t s2 = v.z + __funnelshift_r(v.z, v.w, 8);
-                const uint32_t s3 = v.w + __funnelshift_r(v.w, nx, 8);
-                if ((s0 | s1 | s2 | s3) & pre) {  // rare: exact per-byte test
-                    const uint64_t g0 = tile0 + 16u * (uint32_t)i;
-                    const uint32_t tw = low ? (uint32_t)max(0, bnx_floor2log2(g0 + 1) - 2) : (uint32_t)tt;
-                    const uint32_t T4 = tw * 0x01010101u;
-                    const uint32_t sv[4] = {s0, s1, s2, s3};
+                uint32_t nx = __shfl_down_sync(0xffffffffu, v.x, 1);  // next group's first word
+                if (lane == 31) nx = acc[4 * i + 4];
+                const uint64_t g0 = tile0 + 16u * (uint32_t)i;
+                const uint32_t tw = low ? (uint32_t)max(0, bnx_floor2log2(g0 + 1) - 2) : tt;
+                const uint32_t T4 = tw * 0x01010101u;
+                uint32_t sv[4];
+                sv[0] = v.x + __funnelshift_r(v.x, v.y, 8);  // A(x) + A(x+1), 4 bytes
+                sv[1] = v.y + __funnelshift_r(v.y, v.z, 8);
+                sv[2] = v.z + __funnelshift_r(v.z, v.w, 8);
+                sv[3] = v.w + __funnelshift_r(v.w, nx, 8);
+                uint32_t hit[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) hit[w] = (((sv[w] | 0x80808080u) - T4) | sv[w]) & 0x80808080u;
+                if (hit[0] | hit[1] | hit[2] | hit[3]) {
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
-                        uint32_t m = (((sv[w] | 0x80808080u) - T4) | sv[w]) & 0x80808080u;
+                        uint32_t m = hit[w];
                         while (m) {
                             const int b = (__ffs(m) - 1) >> 3;
                             m &= m - 1;
