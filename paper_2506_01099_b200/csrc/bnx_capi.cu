@@ -220,10 +220,16 @@ int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
         launch_narrow(c->stage64.p, k, c->primes.p, c->stream);
         CK(cudaGetLastError());
     }
-    c->h_primes.resize(k);
-    for (size_t i = 0; i < k; ++i) c->h_primes[i] = (uint32_t)primes[i];
-    c->primes_limit = need;  // the device copy holds exactly the primes <= need
-    c->gen++;
+    // Tables derived from the primes are rebuilt only if the list actually changed (the copy
+    // above always happens: the caller's buffer is the input of every call).
+    bool same = c->gen > 0 && c->h_primes.size() == k && c->primes_limit == need;
+    for (size_t i = 0; same && i < k; ++i) same = c->h_primes[i] == (uint32_t)primes[i];
+    if (!same) {
+        c->h_primes.resize(k);
+        for (size_t i = 0; i < k; ++i) c->h_primes[i] = (uint32_t)primes[i];
+        c->primes_limit = need;  // the device copy holds exactly the primes <= need
+        c->gen++;
+    }
     return BNX_OK;
 }
 
