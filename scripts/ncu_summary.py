@@ -61,6 +61,8 @@ def main():
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--out", default="profiles")
     ap.add_argument("--peak-gbs", type=float, default=6547.5)
+    ap.add_argument("--bytes-per-int", type=float, default=32.0,
+                    help="algorithmic bytes per integer (32: SURVEY 8(d) record model; 8: materialised rad)")
     args = ap.parse_args()
     recs = raw(args.rep)
     rec = recs[0]
@@ -82,8 +84,9 @@ def main():
               f"(SURVEY 8(d) record design: 32 B per integer)",
               f"* {insts / args.integers:.3f} warp instructions per integer "
               f"({32 * insts / args.integers:.2f} thread instructions)",
-              f"* 8(d)-equivalent bandwidth {32 * args.integers / t / 1e9:.0f} GB/s = "
-              f"{32 * args.integers / t / 1e9 / args.peak_gbs:.2f} x measured HBM peak {args.peak_gbs} GB/s"]
+              f"* algorithmic bandwidth ({args.bytes_per_int:g} B/integer) "
+              f"{args.bytes_per_int * args.integers / t / 1e9:.0f} GB/s = "
+              f"{args.bytes_per_int * args.integers / t / 1e9 / args.peak_gbs:.2f} x measured HBM peak {args.peak_gbs} GB/s"]
     if args.launches:
         agg = launches(args.launches)
         total = sum(sum(v) for v in agg.values())
