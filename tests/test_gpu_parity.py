@@ -184,3 +184,41 @@ def test_reference_run_2p32_exact_rows():
     assert rows_of(bp.run_full_chunked(2**32, 2**28)) == ref
     assert sorted(rows_of(bp.find_pairs_sorted(2**32)), key=lambda r: (r[1], r[2])) == \
         sorted(ref, key=lambda r: (r[1], r[2]))
+
+
+@pytest.mark.parametrize("e", [24, 28])
+def test_screen_keeps_every_candidate(orc, e):
+    """The on-chip screen may only over-approximate: the number of n < S with
+    rad(n) rad(n+1) <= 2n that k_tail confirms must equal the exact count from the oracle's
+    sieve (numpy), i.e. no candidate is ever dropped by the log screen."""
+    S = 1 << e
+    vals = orc.sieve_segment(1, S, orc.primes_up_to(math.isqrt(S)))
+    n = np.arange(1, S, dtype=np.uint64)
+    r0, r1 = vals[:-1], vals[1:]
+    exact = int(np.count_nonzero(r0 <= (2 * n) // r1))  # R <= 2n without overflow
+    bp.find_pairs(S)
+    st = bp.last_stats()
+    assert st["candidates"] == exact
+    assert st["survivors"] >= exact
+
+
+def test_random_domains_vs_oracle(orc):
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        lo = int(rng.integers(1, 2_000_000))
+        hi = lo + int(rng.integers(0, 1_000_000))
+        got = [(int(p.kind), p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in bp.search_domain(lo, hi)]
+        want = sorted((r for r in orc.find_pairs_sorted(hi + 1) if r[2] >= lo), key=lambda r: (r[2], r[1]))
+        assert got == want, (lo, hi)
+
+
+def test_near_the_top_of_the_range():
+    """Largest supported bounds (< 2^42): the first-kind family member k = 21,
+    (2^21 - 2, 2^42 - 2^22), lies just below 2^42 and must be found with its radicals."""
+    m, n = 2**21 - 2, 2**42 - 2**22
+    got = bp.search_domain(n - 5000, n + 5000)
+    assert [(int(p.kind), p.m, p.n) for p in got] == [(1, m, n)]
+    p = got[0]
+    assert (p.rad_m, p.rad_m_plus_1) == (bp.radical_oracle(m), bp.radical_oracle(m + 1))
+    with pytest.raises(ValueError):
+        bp.search_domain(2**42 - 10, 2**42)
