@@ -535,28 +535,29 @@ __global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
             }
         }
         __syncthreads();
+        // init: x, or x with all but one factor two removed (_kernels.py:33-45); two integers
+        // per thread and 16-byte stores: exactly one of them is even, and only that one can
+        // need the shift.  Thread g always owns slots 2g, 2g+1 (init, write-out), so the
+        // write-out of tile t and the init of tile t+1 share one pass with no barrier.
+        auto init_pair = [&](uint64_t tile0, int g) {
+            const uint64_t x0 = tile0 + 2u * (uint32_t)g;
+            uint64_t v0 = x0, v1 = x0 + 1;
+            if (a.fast) {
+                const bool odd0 = x0 & 1;
+                const uint64_t xe = odd0 ? v1 : v0;
+                if ((xe & 3) == 0 && xe) {
+                    const uint32_t lo = (uint32_t)xe;
+                    const int tz = lo ? __ffs(lo) - 1 : 31 + __ffs((uint32_t)(xe >> 32));
+                    const uint64_t ve = xe >> (tz - 1);
+                    if (odd0) v1 = ve; else v0 = ve;
+                }
+            }
+            reinterpret_cast<ulonglong2*>(r)[g] = make_ulonglong2(v0, v1);
+        };
+        for (int g = tid; g < TILE / 2; g += THREADS) init_pair(a.start + seg_off, g);
         for (int t = 0; t < NT; ++t) {
             const uint64_t toff = seg_off + (uint64_t)t * TILE;
             if (toff >= a.length) break;
-            const uint64_t tile0 = a.start + toff;
-            // init: x, or x with all but one factor two removed (_kernels.py:33-45); two
-            // integers per thread and 16-byte stores: exactly one of them is even, and only
-            // that one can need the shift.
-            for (int g = tid; g < TILE / 2; g += THREADS) {
-                const uint64_t x0 = tile0 + 2u * (uint32_t)g;
-                uint64_t v0 = x0, v1 = x0 + 1;
-                if (a.fast) {
-                    const bool odd0 = x0 & 1;
-                    const uint64_t xe = odd0 ? v1 : v0;
-                    if ((xe & 3) == 0 && xe) {
-                        const uint32_t lo = (uint32_t)xe;
-                        const int tz = lo ? __ffs(lo) - 1 : 31 + __ffs((uint32_t)(xe >> 32));
-                        const uint64_t ve = xe >> (tz - 1);
-                        if (odd0) v1 = ve; else v0 = ve;
-                    }
-                }
-                reinterpret_cast<ulonglong2*>(r)[g] = make_ulonglong2(v0, v1);
-            }
             __syncthreads();
             // per-tile progressions: balanced work items (see k_screen), exact division per hit
             const int it_end = (int)s_item[warp + 1];
@@ -593,17 +594,20 @@ __global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
                 if (no < 0) no += (int)s_q[j];
                 s_off[j] = (uint32_t)no;
             }
-            // write out: 16-byte streaming stores (the values are not re-read on the device)
+            // write out (16-byte streaming stores; the values are not re-read on the device)
+            // fused with the next tile's init
             const uint64_t rem = a.length - toff;
             const int lim = rem < (uint64_t)TILE ? (int)rem : TILE;
             uint64_t* dst = a.out + toff;
+            const bool next = t + 1 < NT && toff + TILE < a.length;
             if (lim == TILE && ((((uintptr_t)dst) & 15) == 0)) {
-                for (int i = tid; i < TILE / 2; i += THREADS)
-                    __stcs(reinterpret_cast<ulonglong2*>(dst) + i, make_ulonglong2(r[2 * i], r[2 * i + 1]));
+                for (int g = tid; g < TILE / 2; g += THREADS) {
+                    __stcs(reinterpret_cast<ulonglong2*>(dst) + g, reinterpret_cast<const ulonglong2*>(r)[g]);
+                    if (next) init_pair(a.start + toff + TILE, g);
+                }
             } else {
                 for (int i = tid; i < lim; i += THREADS) dst[i] = r[i];
             }
-            __syncthreads();
         }
     }
 }
