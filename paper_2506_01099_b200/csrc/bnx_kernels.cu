@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
     constexpr uint64_t SEG = (uint64_t)TILE * NT;
     extern __shared__ __align__(16) unsigned long long sm64[];
     unsigned long long* r = sm64;                        // TILE slots
-    unsigned long long* bent = r + TILE;                 // NT * BCAP : (prog index << 16 | loc)
+    unsigned long long* bent = r + TILE;                 // NT * BCAP : (p << 16 | loc)
     unsigned long long* s_inv = bent + NT * BCAP;        // MAXS
     uint32_t* bcnt = (uint32_t*)(s_inv + MAXS);          // NT
     uint32_t* s_q = bcnt + NT;                           // MAXS (sorted by q on the host)
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
             while (o < SEG) {
                 const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
                 uint32_t k = atomicAdd(&bcnt[t], 1u);
-                if (k < BCAP) bent[t * BCAP + k] = (j << 16) | loc; else a.flags[0] = 1;
+                if (k < BCAP) bent[t * BCAP + k] = ((uint64_t)pr.p << 16) | loc; else a.flags[0] = 1;
                 if (pr.q >= SEG) break;
                 o += pr.q;
             }
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
                 const uint32_t nb = min(bcnt[t], (uint32_t)BCAP);
                 for (uint32_t i = tid; i < nb; i += THREADS) {
                     const unsigned long long e = bent[t * BCAP + i];
-                    const uint32_t p = a.large[e >> 16].p;
+                    const uint32_t p = (uint32_t)(e >> 16);
                     div_slot(&r[e & 0xFFFFu], p == 2 ? 0ull : bnx_inv64(p), p == 2);
                 }
             }
