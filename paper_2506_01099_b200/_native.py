@@ -290,7 +290,7 @@ _ctx_lock = threading.Lock()
 
 
 def context(device: int | None = None) -> Context:
-    """The process-wide context of `device` (default: the current torch device or 0)."""
+    """The process-wide context of `device` (default: $BNX_DEVICE, else 0)."""
     if device is None:
         device = int(os.environ.get("BNX_DEVICE", "0"))
     with _ctx_lock:
