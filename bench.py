@@ -388,6 +388,26 @@ def run_ours(args) -> None:
         del out
         torch.cuda.empty_cache()
 
+    # ---- the metric's second clause: wall time to S = 2^40 (both kinds, one GPU), checked
+    # against Theorem 1 (20 + 21 pairs); the device search only, tables resident
+    wall40 = None
+    if rank == 0 and world == 1 and not args.no_2p40:
+        S40 = 1 << 40
+        ctx.prepare(S40)
+        ctx.enqueue(1, S40 - 1, 3)
+        ctx.collect()  # warm-up
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.fill_(7)
+        a_ev.record(stream)
+        ctx.enqueue(1, S40 - 1, 3)
+        b_ev.record(stream)
+        rows40 = ctx.collect()
+        exp40 = bp.expected_pairs_up_to(S40)
+        want = sorted((p.m, p.n) for p in exp40.first_kind + exp40.second_kind)
+        wall40 = {"S": S40, "kinds": "both", "wall_s": a_ev.elapsed_time(b_ev) / 1e3,
+                  "int_per_s": (S40 - 1) / (a_ev.elapsed_time(b_ev) / 1e3), "pairs": len(rows40),
+                  "matches_theorem_1": sorted((int(r["m"]), int(r["n"])) for r in rows40) == want}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -439,6 +459,7 @@ def run_ours(args) -> None:
             },
             "cpu_baseline": cpu,
             "sieve_roofline": sieve,
+            "wall_to_2p40": wall40,
             "search_stats": stats,
             "wall_s_timed_region": wall,
         }
@@ -455,6 +476,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sieve", action="store_true", help="skip the secondary radical-sieve roofline")
+    ap.add_argument("--no-2p40", action="store_true", help="skip the wall-time-to-2^40 measurement")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
