@@ -1,0 +1,51 @@
+"""The multi-rank search with real device searches: two ranks (processes) over gloo, both on
+cuda:0 (this environment has one GPU; the ranks' kernels never wait on each other, only the
+final row gather is collective).  Every rank must return the reference's list for 2^24."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, limit, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2506_01099_b200.dist import find_pairs_distributed
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pairs = find_pairs_distributed(limit, device=0)
+    q.put((rank, [(int(p.kind), p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in pairs]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_device_search(world, golden):
+    limit = 1 << 24
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, limit, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [tuple(r) for r in golden["find_pairs_sorted"][str(limit)]]
+    for r in range(world):
+        assert results[r] == want
