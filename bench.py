@@ -361,8 +361,18 @@ def run_ours(args) -> None:
     achieved = BYTES_PER_INT * ints_local / (scr_ms / 1e3) / 1e9
     traffic = load_traffic()
     traffic_bytes = None
+    issue = None
     if traffic and traffic.get("dram_bytes_per_integer") is not None:
         traffic_bytes = traffic["dram_bytes_per_integer"] * ints_local
+    if traffic and traffic.get("warp_inst_per_integer"):
+        # the screen's own limiter: SM instruction issue (4 warp-instructions per SM per clock)
+        props = torch.cuda.get_device_properties(dev)
+        max_mhz = clocks.get("sm_max_mhz") or 1965.0
+        peak_issue = props.multi_processor_count * 4 * max_mhz * 1e6
+        ach_issue = traffic["warp_inst_per_integer"] * ints_local / (scr_ms / 1e3)
+        issue = {"achieved": ach_issue, "peak": peak_issue, "unit": "warp-instructions/s",
+                 "frac": ach_issue / peak_issue,
+                 "inst_per_integer_source": f"ncu {traffic.get('source')} ({traffic['warp_inst_per_integer']:.4f} warp-inst/int)"}
 
     # ---- secondary: the exact radical sieve (radical.py:109-124) materialising rad(x) as
     # uint64 in HBM -- a write-bound kernel, 8 algorithmic bytes per integer
@@ -456,6 +466,7 @@ def run_ours(args) -> None:
                 "screen_ms_per_launch": scr_ms,
                 "pipeline_ms_per_step": sum(pipe_ms) / len(pipe_ms),
                 "screen_share_of_step": scr_ms / ms_local,
+                "issue_roofline": issue,
             },
             "cpu_baseline": cpu,
             "sieve_roofline": sieve,

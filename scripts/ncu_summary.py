@@ -101,6 +101,7 @@ def main():
     if short == "screen":
         with open(os.path.join(args.out, "ncu_screen_traffic.json"), "w") as f:
             json.dump({"dram_bytes_per_integer": per_int, "dram_bytes_per_launch": rd + wr,
+                       "warp_inst_per_integer": insts / args.integers,
                        "integers_per_launch": args.integers, "source": os.path.basename(args.rep),
                        "tag": args.tag}, f, indent=1)
     print("\n".join(lines))
