@@ -6,7 +6,7 @@ Workload (BASELINE.json configs[1]): first-kind search below S = 2^32 on one B20
 the search below S = N * 2^32 (weak scaling, no data-path collective).
 
   value     integers searched / s with the prime tables resident in HBM: per step one
-            device search (k_screen -> k_tail) timed with CUDA events
+            device search (k_screen -> k_tail -> k_tail_heavy) timed with CUDA events
             on the launching stream, L2 flushed (256 MiB write) before every step, max over
             ranks.
   e2e       the same metric through the public API (search_domain with a host PrimeList in
@@ -455,7 +455,7 @@ def run_ours(args) -> None:
             "e2e": {"value": e2e_value, "unit": "n/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms_max,
                     "path": "paper_2506_01099_b200.search.search_rows(primes=PrimeList in pinned memory) -> C ABI bnx_search_domain"},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": stats["kernel_launches"] * args.steps,
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic_bytes, "kernel": "k_screen",

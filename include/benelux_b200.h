@@ -84,6 +84,7 @@ typedef struct bnx_stats {
     uint64_t kernel_launches;/* kernels this library launched for the call            */
     int32_t bucket_overflow; /* nonzero if a tile bucket overflowed (call failed)     */
     int32_t reserved;
+    uint64_t max_residue_checks; /* most residue-class members of a single candidate     */
 } bnx_stats_t;
 
 typedef struct bnx_ctx bnx_ctx_t;

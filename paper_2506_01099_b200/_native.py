@@ -75,6 +75,7 @@ class Stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_uint64),
         ("bucket_overflow", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
+        ("max_residue_checks", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:

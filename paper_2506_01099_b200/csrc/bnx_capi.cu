@@ -118,6 +118,7 @@ struct bnx_ctx {
     Tables screen_tab, sieve_tab, td_tab;
 
     DBuf<uint64_t> surv;
+    DBuf<BnxCand> heavy;
     DBuf<bnx_pair_t> pairs;
     DBuf<unsigned long long> ctr;
     DBuf<int> flags;
@@ -339,6 +340,7 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
 
 int ensure_work(bnx_ctx* c) {
     if (!c->surv.p) TRY(c->surv.ensure(1 << 20));
+    if (!c->heavy.p) TRY(c->heavy.ensure(64));
     if (!c->pairs.p) TRY(c->pairs.ensure(1 << 14));
     TRY(c->ctr.ensure(CTR_N));
     TRY(c->flags.ensure(4));
@@ -363,7 +365,8 @@ int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     sv.launch(sa, sgrid, c->stream);
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
-    TailArgs ta{c->surv.p, c->surv.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap, c->ctr.p};
+    TailArgs ta{c->surv.p, c->surv.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap,
+                c->ctr.p};
     launch_tail(ta, grid_for(c), c->stream);
     CK(cudaGetLastError());
     if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
@@ -375,7 +378,7 @@ int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     c->q_kinds = kinds;
     c->stats = bnx_stats_t{};
     c->stats.integers = n_last - n_first + 1;
-    c->stats.kernel_launches = 2;
+    c->stats.kernel_launches = 3;
     return BNX_OK;
 }
 
@@ -399,6 +402,7 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
         const unsigned long long* h = c->h_ctr;
         bool again = false;
         if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
+        if (h[CTR_HEAVY] > c->heavy.cap) { TRY(c->heavy.ensure(h[CTR_HEAVY] * 2)); again = true; }
         if (h[CTR_PAIRS] > c->pairs.cap) { TRY(c->pairs.ensure(h[CTR_PAIRS] * 2)); again = true; }
         if (again) {
             TRY(enqueue(c, c->q_first, c->q_last, c->q_kinds));
@@ -414,6 +418,7 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
         c->stats.candidates = h[CTR_CAND];
         c->stats.residue_checks = h[CTR_CHECKS];
         c->stats.matches = h[CTR_MATCH];
+        c->stats.max_residue_checks = h[CTR_MAXCHK];
         c->stats.pairs = np;
         if (c->timing) {
             CK(cudaEventElapsedTime(&c->screen_ms, c->ev[0], c->ev[1]));
@@ -499,6 +504,7 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->sieve_tab.release();
     c->td_tab.release();
     c->surv.release();
+    c->heavy.release();
     c->pairs.release();
     c->ctr.release();
     c->flags.release();

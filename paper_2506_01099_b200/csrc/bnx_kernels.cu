@@ -428,54 +428,115 @@ __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_
 //     radicals, tested exactly: rad(m) == r  <=>  r | m  and  m / r | r^inf (gcds).
 //  3. every kept m is verified by full radical comparison (rad_warp of m and m+1) and
 //     classified as the reference does (signatures.py:67-81), then emitted.
-__global__ void __launch_bounds__(256) k_tail(TailArgs a) {
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// One candidate n (R = r0 r1 <= 2n) and a range [k_begin, k_end) of its residue-class members:
+// k < t1 -> first kind m = n - (k+1) R; else second kind m = (t0 + k - t1) R - n - 1.  With
+// s0 = n / r0 and s1 = (n+1) / r1 the cofactors are linear in t, so no division is needed:
+//   first kind   m / r0 = s0 - t r1,   (m+1) / r1 = s1 - t r0
+//   second kind  m / r1 = t r0 - s1,   (m+1) / r0 = t r1 - s0
+// and m is kept iff both cofactors are supported by their radical (u | r^inf).  Kept m are
+// verified by full radical comparison and classified (signatures.py:67-81).  Warp-collective.
+struct TailCand {
+    uint64_t n, r0, r1, R, s0, s1, t0, t1;
+};
+
+__device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_begin, uint64_t k_end) {
     const int lane = threadIdx.x & 31;
-    const uint64_t cnt = min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
-    for (uint64_t i = gw; i < cnt; i += nwarps) {
-        const uint64_t n = a.surv[i];
-        const uint64_t r0 = rad_warp(n, a.pdiv, a.npdiv);
-        const uint64_t r1 = rad_warp(n + 1, a.pdiv, a.npdiv);
-        if (__umul64hi(r0, r1) != 0 || r0 * r1 > 2 * n) continue;  // warp-uniform
-        const uint64_t R = r0 * r1;
-        const uint64_t t1 = (a.kinds & 1u) ? (n - 1) / R : 0;            // m = n - tR >= 1
-        const uint64_t t0 = (n + 1) / R + 1, t2 = (2 * n) / R;             // n + 2 <= tR <= 2n
-        const uint64_t c2 = ((a.kinds & 2u) && t2 >= t0) ? t2 - t0 + 1 : 0;
-        const uint64_t total = t1 + c2;
-        if (lane == 0) {
-            atomicAdd(&a.ctr[CTR_CAND], 1ull);
-            if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
-        }
-        for (uint64_t base = 0; base < total; base += 32) {
-            const uint64_t k = base + lane;
-            uint64_t m = 0;
-            bool ok = false;
-            if (k < total) {
-                uint64_t ra, rb;
-                if (k < t1) { m = n - (k + 1) * R; ra = r0; rb = r1; }
-                else { m = (t0 + (k - t1)) * R - n - 1; ra = r1; rb = r0; }
-                ok = m % ra == 0 && (m + 1) % rb == 0 && bnx_supported_by(m / ra, ra) && bnx_supported_by((m + 1) / rb, rb);
+    for (uint64_t base = k_begin; base < k_end; base += 32) {
+        const uint64_t k = base + lane;
+        uint64_t m = 0;
+        bool ok = false;
+        if (k < k_end) {
+            if (k < c.t1) {
+                const uint64_t t = k + 1;
+                m = c.n - t * c.R;
+                ok = bnx_supported_by(c.s0 - t * c.r1, c.r0) && bnx_supported_by(c.s1 - t * c.r0, c.r1);
+            } else {
+                const uint64_t t = c.t0 + (k - c.t1);
+                m = t * c.R - c.n - 1;
+                ok = bnx_supported_by(t * c.r0 - c.s1, c.r1) && bnx_supported_by(t * c.r1 - c.s0, c.r0);
             }
-            uint32_t bal = __ballot_sync(0xffffffffu, ok);
-            while (bal) {
-                const int src = __ffs(bal) - 1;
-                bal &= bal - 1;
-                const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
-                const uint64_t rm = rad_warp(mm, a.pdiv, a.npdiv), rm1 = rad_warp(mm + 1, a.pdiv, a.npdiv);
-                int kind = 0;
-                if (rm == r0 && rm1 == r1) kind = 1;
-                else if (rm == r1 && rm1 == r0) kind = 2;
-                if (lane == 0) {
-                    atomicAdd(&a.ctr[CTR_MATCH], 1ull);
-                    if (kind && (a.kinds & (1u << (kind - 1))) && mm >= 1 && mm < n) {
-                        unsigned long long s = atomicAdd(&a.ctr[CTR_PAIRS], 1ull);
-                        if (s < a.pair_cap) a.pairs[s] = bnx_pair_t{mm, n, rm, rm1, kind, 0};
-                    }
+        }
+        uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        while (bal) {
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
+            const uint64_t rm = rad_warp(mm, a.pdiv, a.npdiv), rm1 = rad_warp(mm + 1, a.pdiv, a.npdiv);
+            int kind = 0;
+            if (rm == c.r0 && rm1 == c.r1) kind = 1;
+            else if (rm == c.r1 && rm1 == c.r0) kind = 2;
+            if (lane == 0) {
+                atomicAdd(&a.ctr[CTR_MATCH], 1ull);
+                if (kind && (a.kinds & (1u << (kind - 1))) && mm >= 1 && mm < c.n) {
+                    unsigned long long s = atomicAdd(&a.ctr[CTR_PAIRS], 1ull);
+                    if (s < a.pair_cap) a.pairs[s] = bnx_pair_t{mm, c.n, rm, rm1, kind, 0};
                 }
             }
         }
     }
+}
+
+// Candidates with more than this many residue-class members are handed to k_tail_heavy,
+// which spreads their members over many warps (one candidate below 2^32 has ~1,500).
+constexpr uint64_t TAIL_HEAVY = 128;
+
+__global__ void __launch_bounds__(256) k_tail(TailArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t cnt = min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
+    for (;;) {
+        // survivors are taken one at a time from a shared counter
+        unsigned long long i = 0;
+        if (lane == 0) i = atomicAdd(&a.ctr[CTR_NEXT], 1ull);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= cnt) break;
+        const uint64_t n = a.surv[i];
+        const uint64_t r0 = rad_warp(n, a.pdiv, a.npdiv);
+        const uint64_t r1 = rad_warp(n + 1, a.pdiv, a.npdiv);
+        if (__umul64hi(r0, r1) != 0 || r0 * r1 > 2 * n) continue;  // warp-uniform
+        TailCand c;
+        c.n = n; c.r0 = r0; c.r1 = r1; c.R = r0 * r1;
+        c.s0 = n / r0; c.s1 = (n + 1) / r1;
+        c.t1 = (a.kinds & 1u) ? (n - 1) / c.R : 0;          // m = n - tR >= 1
+        c.t0 = (n + 1) / c.R + 1;                            // n + 2 <= tR <= 2n
+        const uint64_t t2 = (2 * n) / c.R;
+        const uint64_t c2 = ((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0;
+        const uint64_t total = c.t1 + c2;
+        if (lane == 0) {
+            atomicAdd(&a.ctr[CTR_CAND], 1ull);
+            if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
+            atomicMax(&a.ctr[CTR_MAXCHK], (unsigned long long)total);
+        }
+        if (total > TAIL_HEAVY) {
+            bool queued = false;
+            if (lane == 0) {
+                const unsigned long long h = atomicAdd(&a.ctr[CTR_HEAVY], 1ull);
+                if (h < a.heavy_cap) {
+                    a.heavy[h] = BnxCand{n, r0, r1};
+                    queued = true;
+                }
+            }
+            if (__shfl_sync(0xffffffffu, (int)queued, 0)) continue;
+        }
+        tail_members(a, c, 0, total);
+    }
+}
+
+// Heavy candidates: blockIdx.y picks the candidate, the warps of the x-blocks split its members
+// into chunks of 32.
+__global__ void __launch_bounds__(256) k_tail_heavy(TailArgs a) {
+    const uint64_t nh = min((uint64_t)a.ctr[CTR_HEAVY], a.heavy_cap);
+    if (blockIdx.y >= nh) return;
+    const BnxCand h = a.heavy[blockIdx.y];
+    TailCand c;
+    c.n = h.n; c.r0 = h.r0; c.r1 = h.r1; c.R = h.r0 * h.r1;
+    c.s0 = h.n / h.r0; c.s1 = (h.n + 1) / h.r1;
+    c.t1 = (a.kinds & 1u) ? (h.n - 1) / c.R : 0;
+    c.t0 = (h.n + 1) / c.R + 1;
+    const uint64_t t2 = (2 * h.n) / c.R;
+    const uint64_t total = c.t1 + (((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0);
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t chunk = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); chunk * 32 < total; chunk += nwarps)
+        tail_members(a, c, chunk * 32, min(total, chunk * 32 + 32));
 }
 
 // ------------------------------------------------------------------------------------
@@ -773,7 +834,10 @@ void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st) {
     k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>
         <<<grid, SIEVE_THREADS, sieve_smem_bytes(), st>>>(a);
 }
-void launch_tail(const TailArgs& a, int grid, cudaStream_t st) { k_tail<<<grid, 256, 0, st>>>(a); }
+void launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
+    k_tail<<<grid, 256, 0, st>>>(a);
+    k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);
+}
 
 void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st) {
     if (ls + 1 > 48 * 1024) cudaFuncSetAttribute(k_base_primes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ls + 1));

@@ -19,7 +19,10 @@ constexpr int SIEVE_BCAP = 64;
 constexpr int SIEVE_MAXS = 160;
 
 // Counter block (device): [0] survivors [1] candidates [2] residue checks [3] matches [4] pairs
-constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_N = 8;
+// [5] the tail's work queue head [6] most residue-class members of one candidate
+// [7] heavy candidates queued for k_tail_heavy
+constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_NEXT = 5, CTR_MAXCHK = 6,
+              CTR_HEAVY = 7, CTR_N = 8;
 
 struct ScreenArgs {
     uint64_t x_begin;  // multiple of the tile
@@ -41,6 +44,8 @@ struct ScreenArgs {
 struct TailArgs {
     const uint64_t* surv;
     uint64_t surv_cap;
+    BnxCand* heavy;      // candidates with many residue-class members
+    uint64_t heavy_cap;
     const BnxPDiv* pdiv;
     uint64_t npdiv;
     uint32_t kinds;
