@@ -428,6 +428,61 @@ __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_
 //     radicals, tested exactly: rad(m) == r  <=>  r | m  and  m / r | r^inf (gcds).
 //  3. every kept m is verified by full radical comparison (rad_warp of m and m+1) and
 //     classified as the reference does (signatures.py:67-81), then emitted.
+// rad(x) and rad(x+1) in one warp-cooperative pass (same method as rad_warp): each lane
+// tests its primes against both odd parts, so the two chains overlap.
+__device__ void rad2_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_t npd, uint64_t& rx, uint64_t& rx1) {
+    const int lane = threadIdx.x & 31;
+    const int tz0 = bnx_ctz64(x), tz1 = bnx_ctz64(x + 1);
+    const uint64_t y0 = x >> tz0, y1 = (x + 1) >> tz1;
+    const uint64_t ymax = y0 > y1 ? y0 : y1;
+    uint64_t pr0 = 1, pp0 = 1, pr1 = 1, pp1 = 1;
+    bool go = true;
+    for (uint64_t j = lane; go && j < npd; j += 128) {
+        BnxPDiv d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t jj = j + 32u * u;
+            d[u] = jj < npd ? pd[jj] : BnxPDiv{1ull << 21, 0, 0};  // sentinel: p^3 = 2^63 > y
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (d[u].p * d[u].p * d[u].p > ymax) { go = false; break; }
+            uint64_t t = y0 * d[u].inv;
+            if (t <= d[u].lim) {
+                pr0 *= d[u].p;
+                pp0 *= d[u].p;
+                while (t * d[u].inv <= d[u].lim) { t *= d[u].inv; pp0 *= d[u].p; }
+            }
+            t = y1 * d[u].inv;
+            if (t <= d[u].lim) {
+                pr1 *= d[u].p;
+                pp1 *= d[u].p;
+                while (t * d[u].inv <= d[u].lim) { t *= d[u].inv; pp1 *= d[u].p; }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        pr0 *= __shfl_xor_sync(0xffffffffu, pr0, o);
+        pp0 *= __shfl_xor_sync(0xffffffffu, pp0, o);
+        pr1 *= __shfl_xor_sync(0xffffffffu, pr1, o);
+        pp1 *= __shfl_xor_sync(0xffffffffu, pp1, o);
+    }
+    auto finish = [](uint64_t y, uint64_t pr, uint64_t pp, int tz) {
+        const uint64_t c = y * bnx_inv64(pp);
+        uint64_t rc = c;
+        if (c > 1) {
+            uint64_t sq = (uint64_t)sqrt((double)c);
+            while (sq * sq > c) --sq;
+            while ((sq + 1) * (sq + 1) <= c) ++sq;
+            if (sq * sq == c) rc = sq;
+        }
+        return (tz ? 2ull : 1ull) * pr * rc;
+    };
+    rx = finish(y0, pr0, pp0, tz0);
+    rx1 = finish(y1, pr1, pp1, tz1);
+}
+
 // One candidate n (R = r0 r1 <= 2n) and a range [k_begin, k_end) of its residue-class members:
 // k < t1 -> first kind m = n - (k+1) R; else second kind m = (t0 + k - t1) R - n - 1.  With
 // s0 = n / r0 and s1 = (n+1) / r1 the cofactors are linear in t, so no division is needed:
@@ -461,7 +516,8 @@ __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_be
             const int src = __ffs(bal) - 1;
             bal &= bal - 1;
             const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
-            const uint64_t rm = rad_warp(mm, a.pdiv, a.npdiv), rm1 = rad_warp(mm + 1, a.pdiv, a.npdiv);
+            uint64_t rm, rm1;
+            rad2_warp(mm, a.pdiv, a.npdiv, rm, rm1);
             int kind = 0;
             if (rm == c.r0 && rm1 == c.r1) kind = 1;
             else if (rm == c.r1 && rm1 == c.r0) kind = 2;
@@ -490,8 +546,8 @@ __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
         i = __shfl_sync(0xffffffffu, i, 0);
         if (i >= cnt) break;
         const uint64_t n = a.surv[i];
-        const uint64_t r0 = rad_warp(n, a.pdiv, a.npdiv);
-        const uint64_t r1 = rad_warp(n + 1, a.pdiv, a.npdiv);
+        uint64_t r0, r1;
+        rad2_warp(n, a.pdiv, a.npdiv, r0, r1);
         if (__umul64hi(r0, r1) != 0 || r0 * r1 > 2 * n) continue;  // warp-uniform
         TailCand c;
         c.n = n; c.r0 = r0; c.r1 = r1; c.R = r0 * r1;
