@@ -318,15 +318,18 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
     if (ns > small_cap) return fail(BNX_ERR_CUDA, "too many small progressions");
     std::vector<BnxProg> hs(ns);
     if (ns) {
-        CK(cudaMemcpy(hs.data(), t.small.p, sizeof(BnxProg) * ns, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(hs.data(), t.small.p, sizeof(BnxProg) * ns, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
         std::sort(hs.begin(), hs.end(), [](const BnxProg& x, const BnxProg& y) { return x.q < y.q; });
-        CK(cudaMemcpy(t.small.p, hs.data(), sizeof(BnxProg) * ns, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(t.small.p, hs.data(), sizeof(BnxProg) * ns, cudaMemcpyHostToDevice, c->stream));
     }
     std::vector<uint32_t> items = build_items(hs, tile, nwarps);
     if (items.size() > 2 * (size_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many screen work items");
     TRY(t.items.ensure(items.size() + 1));
     if (!items.empty())
-        CK(cudaMemcpy(t.items.p, items.data(), sizeof(uint32_t) * items.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(t.items.p, items.data(), sizeof(uint32_t) * items.size(), cudaMemcpyHostToDevice,
+                           c->stream));
+    CK(cudaStreamSynchronize(c->stream));  // the host vectors above must outlive the copies
     t.nitems = (int)items.size();
     t.nsmall = ns;
     t.nlarge = nl;
