@@ -349,13 +349,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
                 sv[1] = v.y + __funnelshift_r(v.y, v.z, 8);
                 sv[2] = v.z + __funnelshift_r(v.z, v.w, 8);
                 sv[3] = v.w + __funnelshift_r(v.w, nx, 8);
-                uint32_t hit[4];
+                // byte b passes iff bit 7 of ((s | 0x80) - T) | s is set; OR the four words
+                // first and mask once (the other bits are don't-care)
+                uint32_t any = 0;
 #pragma unroll
-                for (int w = 0; w < 4; ++w) hit[w] = (((sv[w] | 0x80808080u) - T4) | sv[w]) & 0x80808080u;
-                if (hit[0] | hit[1] | hit[2] | hit[3]) {
+                for (int w = 0; w < 4; ++w) any |= ((sv[w] | 0x80808080u) - T4) | sv[w];
+                if (any & 0x80808080u) {
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
-                        uint32_t m = hit[w];
+                        uint32_t m = (((sv[w] | 0x80808080u) - T4) | sv[w]) & 0x80808080u;
                         while (m) {
                             const int b = (__ffs(m) - 1) >> 3;
                             m &= m - 1;
