@@ -99,9 +99,17 @@ BNX_API int bnx_ctx_destroy(bnx_ctx_t* ctx);
 BNX_API int bnx_ctx_set_stream(bnx_ctx_t* ctx, void* stream);
 BNX_API int bnx_ctx_stats(const bnx_ctx_t* ctx, bnx_stats_t* out);
 /* Kernel timing with CUDA events on the context stream: when enabled, each search records
- * events around the screen kernel and around the whole device pipeline; bnx_ctx_timing
+ * events around the candidate generator (screen) and around the whole device pipeline; bnx_ctx_timing
  * returns the last search's milliseconds (valid after bnx_search_collect / bnx_search*). */
 BNX_API int bnx_ctx_set_timing(bnx_ctx_t* ctx, int enabled);
+/* Candidate generator of the search (results are identical):
+ * BNX_ENGINE_HEAVY (default) lists the heavy integers (2 s(x)^2 >= x, s = x / rad x) and tests
+ * their neighbours; BNX_ENGINE_SCREEN sieves a log-surplus byte per integer.  The environment
+ * variable BNX_ENGINE=screen selects the screen at context creation. */
+#define BNX_ENGINE_HEAVY 0
+#define BNX_ENGINE_SCREEN 1
+BNX_API int bnx_ctx_set_engine(bnx_ctx_t* ctx, int engine);
+BNX_API int bnx_ctx_engine(const bnx_ctx_t* ctx);
 BNX_API int bnx_ctx_timing(const bnx_ctx_t* ctx, float* screen_ms, float* pipeline_ms);
 
 /* primes.py:24-35: all primes <= limit, ascending.  *count always receives the total;

@@ -24,11 +24,12 @@ BNX_ERR_CUDA = 5
 BNX_ERR_RANGE = 6
 
 KIND_FIRST, KIND_SECOND, KIND_BOTH = 1, 2, 3
+ENGINES = {"heavy": 0, "screen": 1}  # bnx_ctx_set_engine (include/benelux_b200.h)
 
 # Every symbol include/benelux_b200.h declares (tests check the library exports them all).
 EXPORTED_SYMBOLS = (
     "bnx_version", "bnx_last_error", "bnx_device_count", "bnx_ctx_create", "bnx_ctx_destroy",
-    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_primes_up_to", "bnx_sieve_radicals",
+    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_primes_up_to", "bnx_sieve_radicals",
     "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain",
     "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of", "bnx_brute_force",
     "bnx_table_create", "bnx_table_destroy", "bnx_table_insert_all", "bnx_table_probe_all", "bnx_table_slots",
@@ -109,6 +110,8 @@ def load() -> ctypes.CDLL:
         L.bnx_ctx_set_stream.argtypes = [vp, vp]
         L.bnx_ctx_stats.argtypes = [vp, ctypes.POINTER(Stats)]
         L.bnx_ctx_set_timing.argtypes = [vp, ctypes.c_int]
+        L.bnx_ctx_set_engine.argtypes = [vp, ctypes.c_int]
+        L.bnx_ctx_engine.argtypes = [vp]
         L.bnx_ctx_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
         L.bnx_primes_up_to.argtypes = [vp, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_sieve_radicals.argtypes = [
@@ -195,6 +198,16 @@ class Context:
     def set_timing(self, enabled: bool) -> None:
         with self.lock:
             check(load().bnx_ctx_set_timing(self.handle, int(bool(enabled))))
+
+    def set_engine(self, engine: str | int) -> None:
+        """Candidate generator: "heavy" (default) or "screen" (identical results)."""
+        code = ENGINES[engine] if isinstance(engine, str) else int(engine)
+        with self.lock:
+            check(load().bnx_ctx_set_engine(self.handle, code))
+
+    def engine(self) -> str:
+        code = load().bnx_ctx_engine(self.handle)
+        return {v: k for k, v in ENGINES.items()}.get(code, str(code))
 
     def timing(self) -> tuple[float, float]:
         """(screen kernel ms, whole device pipeline ms) of the last search (CUDA events)."""

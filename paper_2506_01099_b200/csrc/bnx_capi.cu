@@ -96,6 +96,32 @@ struct Tables {
     }
 };
 
+// Heavy-side generator tables (bnx_heavy.cu): the surplus classes of every powerful number
+// b <= max_x, the per-k bit table, and the per-search scratch (counts, scan).
+struct HeavyTab {
+    uint64_t max_x = 0;
+    uint64_t gen = ~0ull;
+    DBuf<BnxHeavyEnt> ent;
+    uint64_t nent = 0;
+    DBuf<uint32_t> kinfo;
+    uint64_t nkinfo = 0;
+    DBuf<uint64_t> cnt, incl;
+    DBuf<uint32_t> klo;
+    DBuf<unsigned char> scan_temp;
+    size_t scan_bytes = 0;
+    std::vector<uint64_t> sigma;  // host mirror: sigma of each class, ascending
+    void release() {
+        ent.release();
+        kinfo.release();
+        cnt.release();
+        incl.release();
+        klo.release();
+        scan_temp.release();
+        gen = ~0ull;
+        max_x = 0;
+    }
+};
+
 }  // namespace
 
 struct bnx_ctx {
@@ -116,6 +142,10 @@ struct bnx_ctx {
     DBuf<uint64_t> stage64;
 
     Tables screen_tab, sieve_tab, td_tab;
+    HeavyTab heavy_tab;
+    int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
+    DBuf<ulonglong2> q1;
+    DBuf<BnxCand> cand;
 
     DBuf<uint64_t> surv;
     DBuf<BnxCand> heavy;
@@ -341,6 +371,73 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
     return BNX_OK;
 }
 
+// The surplus classes: every powerful b = prod p^(e+1) <= max_x (DFS over the primes up to
+// sqrt(max_x)) with sigma = prod p^e = m r, r = prod p; and kinfo[k] for k <= sqrt(max_x / 2)
+// (the largest k any class can use: k^2 <= 2m * max_x / (m r^2) <= max_x / 2 for r >= 2).
+int build_heavy(bnx_ctx* c, uint64_t max_x) {
+    HeavyTab& h = c->heavy_tab;
+    if (h.gen == c->gen && h.max_x >= max_x) return BNX_OK;
+    const std::vector<uint32_t>& P = c->h_primes;
+    const uint64_t root = isqrt_u64(max_x);
+    if (P.empty() || (P.back() < root && c->primes_limit < root))
+        return fail(BNX_ERR_PRIMES_UNCOVERED, "prime table does not cover sqrt(bound)");
+    std::vector<BnxHeavyEnt> ents;
+    ents.reserve((size_t)(2.5 * std::sqrt((double)max_x)) + 64);
+    struct Node { uint64_t b, sigma, r; uint32_t rmask, rbig, rbig_min; size_t next; };
+    std::vector<Node> stack;
+    stack.push_back(Node{1, 1, 1, 0, 1, 0, 0});
+    while (!stack.empty()) {
+        const Node f = stack.back();
+        stack.pop_back();
+        ents.push_back(BnxHeavyEnt{f.b, f.sigma / f.r, (uint32_t)f.r, f.rmask, f.rbig, f.rbig_min});
+        for (size_t i = f.next; i < P.size(); ++i) {
+            const uint64_t p = P[i];
+            if (p > root || f.b > max_x / (p * p)) break;
+            Node ch{f.b * p * p, f.sigma * p, f.r * p, f.rmask, f.rbig, f.rbig_min, i + 1};
+            if (i < 31) ch.rmask |= 1u << i;
+            else {
+                ch.rbig = (uint32_t)(f.rbig * p);
+                if (!ch.rbig_min) ch.rbig_min = (uint32_t)p;
+            }
+            for (;;) {
+                stack.push_back(ch);
+                if (ch.b > max_x / p) break;
+                ch.b *= p;
+                ch.sigma *= p;
+            }
+        }
+    }
+    // by sigma: a domain [x_lo, x_hi] only needs the classes with 2 sigma^2 >= x_lo (a suffix)
+    std::sort(ents.begin(), ents.end(),
+              [](const BnxHeavyEnt& u, const BnxHeavyEnt& v) { return u.m * u.r < v.m * v.r; });
+    h.sigma.resize(ents.size());
+    for (size_t i = 0; i < ents.size(); ++i) h.sigma[i] = ents[i].m * ents[i].r;
+    const uint64_t K = isqrt_u64(max_x / 2) + 3;
+    std::vector<uint32_t> kinfo(K, 0);
+    for (size_t i = 0; i < 31 && i < P.size(); ++i)
+        for (uint64_t k = P[i]; k < K; k += P[i]) kinfo[k] |= 1u << i;
+    for (size_t i = 0; i < P.size() && (uint64_t)P[i] * P[i] < K; ++i) {
+        const uint64_t q = (uint64_t)P[i] * P[i];
+        for (uint64_t k = q; k < K; k += q) kinfo[k] |= 0x80000000u;
+    }
+    kinfo[0] = 0x80000000u;
+    TRY(h.ent.ensure(ents.size()));
+    TRY(h.kinfo.ensure(K));
+    TRY(h.cnt.ensure(ents.size()));
+    TRY(h.incl.ensure(ents.size()));
+    TRY(h.klo.ensure(ents.size()));
+    h.scan_bytes = heavy_scan_temp_bytes(ents.size());
+    TRY(h.scan_temp.ensure(h.scan_bytes));
+    CK(cudaMemcpyAsync(h.ent.p, ents.data(), sizeof(BnxHeavyEnt) * ents.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(h.kinfo.p, kinfo.data(), sizeof(uint32_t) * K, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));  // the host vectors must outlive the copies
+    h.nent = ents.size();
+    h.nkinfo = K;
+    h.max_x = max_x;
+    h.gen = c->gen;
+    return BNX_OK;
+}
+
 int ensure_work(bnx_ctx* c) {
     if (!c->surv.p) TRY(c->surv.ensure(1 << 20));
     if (!c->heavy.p) TRY(c->heavy.ensure(64));
@@ -354,7 +451,83 @@ int ensure_work(bnx_ctx* c) {
 
 int grid_for(bnx_ctx* c) { return c->num_sms * 4; }
 
+uint64_t iroot4_u64(uint64_t x) {
+    uint64_t r = isqrt_u64(isqrt_u64(x));
+    while ((r + 1) * (r + 1) * (r + 1) * (r + 1) <= x) ++r;
+    return r;
+}
+
+// Heavy engine: k_heavy_count, scan, k_heavy_screen, k_heavy_exact, then the tail on the
+// exact candidates.
+int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
+    HeavyTab& h = c->heavy_tab;
+    Tables& t = c->screen_tab;  // pdiv: odd primes <= sqrt(bound)
+    TRY(ensure_work(c));
+    if (!c->q1.p) TRY(c->q1.ensure(1 << 20));
+    if (!c->cand.p) TRY(c->cand.ensure(1 << 16));
+    const uint64_t y_max = n_last + 2;
+    const uint64_t p2 = iroot4_u64(y_max), p3 = icbrt_u64(y_max);
+    auto odd_upto = [&](uint64_t v) -> uint64_t {  // odd primes <= v in the host table
+        const uint64_t all = (uint64_t)(std::upper_bound(c->h_primes.begin(), c->h_primes.end(),
+                                                         (uint32_t)std::min<uint64_t>(v, 0xFFFFFFFFull)) -
+                                        c->h_primes.begin());
+        return (all && c->h_primes[0] == 2) ? all - 1 : all;
+    };
+    const uint64_t np2 = std::min<uint64_t>(odd_upto(p2), t.npdiv), np3 = std::min<uint64_t>(odd_upto(p3), t.npdiv);
+    if (np2 > (uint64_t)HEAVY_NP2 || np3 > (uint64_t)HEAVY_NP3)
+        return fail(BNX_ERR_RANGE, "bound too large for the heavy generator");
+    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+    CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+    HeavyArgs ha{};
+    // first class with 2 sigma^2 >= n_first (smaller sigma have no heavy x in the domain)
+    const uint64_t smin = isqrt_u64(n_first / 2);
+    const uint64_t start = (uint64_t)(std::lower_bound(h.sigma.begin(), h.sigma.end(), smin) - h.sigma.begin());
+    ha.ent = h.ent.p + start;
+    ha.nent = h.nent - start;
+    ha.cnt = h.cnt.p;
+    ha.incl = h.incl.p;
+    ha.klo = h.klo.p;
+    ha.kinfo = h.kinfo.p;
+    ha.nkinfo = h.nkinfo;
+    ha.x_lo = n_first;
+    ha.x_hi = n_last + 1;
+    ha.n_first = n_first;
+    ha.n_last = n_last;
+    ha.pdiv = t.pdiv.p;
+    ha.np2 = (int)np2;
+    ha.np3 = np3;
+    ha.p1 = p2 + 1;
+    ha.p1sq = ha.p1 * ha.p1;
+    ha.p1cube = ha.p1sq * ha.p1;
+    ha.inv_p1f = 1.0f / (float)ha.p1;
+    ha.cube_filter = p2 >= 7;
+    ha.q1 = c->q1.p;
+    ha.q1_cap = c->q1.cap;
+    ha.cand = c->cand.p;
+    ha.cand_cap = c->cand.cap;
+    ha.ctr = c->ctr.p;
+    ha.flags = c->flags.p;
+    if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
+    launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * 8, c->stream, c->timing ? c->ev[1] : nullptr);
+    TailArgs ta{nullptr, 0, c->cand.p, c->cand.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p,
+                c->pairs.cap, c->ctr.p};
+    launch_tail(ta, grid_for(c), c->stream);
+    CK(cudaGetLastError());
+    if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+    CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    c->q_valid = true;
+    c->q_first = n_first;
+    c->q_last = n_last;
+    c->q_kinds = kinds;
+    c->stats = bnx_stats_t{};
+    c->stats.integers = n_last - n_first + 1;
+    c->stats.kernel_launches = ha.nent ? 7 : 3;  // count, scan (2), screen, exact, tail, tail_heavy
+    return BNX_OK;
+}
+
 int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
+    if (c->engine == 0) return enqueue_heavy(c, n_first, n_last, kinds);
     Tables& t = c->screen_tab;
     TRY(ensure_work(c));
     const ScreenVariant& sv = screen_variant(c->screen_v);
@@ -368,7 +541,7 @@ int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     sv.launch(sa, sgrid, c->stream);
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
-    TailArgs ta{c->surv.p, c->surv.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap,
+    TailArgs ta{c->surv.p, c->surv.cap, nullptr, 0, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap,
                 c->ctr.p};
     launch_tail(ta, grid_for(c), c->stream);
     CK(cudaGetLastError());
@@ -393,6 +566,7 @@ int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint6
                      screen_variant(c->screen_v).threads / 32));
 
     if (c->screen_tab.nsmall > (uint32_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
+    if (c->engine == 0) TRY(build_heavy(c, max_x));
     return BNX_OK;
 }
 
@@ -404,7 +578,11 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
         if (c->h_flags[0]) return fail(BNX_ERR_CUDA, "screen bucket overflow");
         const unsigned long long* h = c->h_ctr;
         bool again = false;
-        if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
+        if (c->h_flags[1]) return fail(BNX_ERR_CUDA, "heavy generator: k outside its table");
+        if (c->engine == 0) {
+            if (h[CTR_SURV] > c->q1.cap) { TRY(c->q1.ensure(h[CTR_SURV] * 2)); again = true; }
+            if (h[CTR_CAND] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_CAND] * 2)); again = true; }
+        } else if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
         if (h[CTR_HEAVY] > c->heavy.cap) { TRY(c->heavy.ensure(h[CTR_HEAVY] * 2)); again = true; }
         if (h[CTR_PAIRS] > c->pairs.cap) { TRY(c->pairs.ensure(h[CTR_PAIRS] * 2)); again = true; }
         if (again) {
@@ -479,6 +657,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     c->own_stream = true;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
+    if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
     if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
         const int v = std::atoi(env);
         if (v >= 0 && v < screen_variant_count()) c->screen_v = v;
@@ -506,6 +685,9 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->screen_tab.release();
     c->sieve_tab.release();
     c->td_tab.release();
+    c->heavy_tab.release();
+    c->q1.release();
+    c->cand.release();
     c->surv.release();
     c->heavy.release();
     c->pairs.release();
@@ -557,6 +739,16 @@ int bnx_ctx_set_timing(bnx_ctx_t* c, int enabled) {
     c->timing = enabled != 0;
     return BNX_OK;
 }
+
+int bnx_ctx_set_engine(bnx_ctx_t* c, int engine) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (engine != BNX_ENGINE_HEAVY && engine != BNX_ENGINE_SCREEN) return fail(BNX_ERR_INVALID, "unknown engine");
+    if (c->q_valid) return fail(BNX_ERR_INVALID, "a search is enqueued");
+    c->engine = engine;
+    return BNX_OK;
+}
+
+int bnx_ctx_engine(const bnx_ctx_t* c) { return c ? c->engine : -1; }
 
 int bnx_ctx_timing(const bnx_ctx_t* c, float* screen_ms, float* pipeline_ms) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");

@@ -1,0 +1,336 @@
+// bnx_heavy.cu -- the candidate generator of the search: heavy-side enumeration.
+//
+// A candidate is an n with R = rad(n) rad(n+1) <= 2n (Lemma 1).  With the
+// surplus s(x) = x / rad(x) that reads  s(n) s(n+1) >= (n+1)/2, so the larger surplus is at
+// least sqrt((n+1)/2): one of x in {n, n+1} is HEAVY, 2 s(x)^2 >= x.  Heavy integers are
+// rare (about 50 sqrt(N) below N) and can be listed without looking at the others:
+//   x = k * sigma * rad(sigma),  sigma = s(x),  k = the squarefree part of x (coprime to
+//   sigma),  and  x heavy  <=>  k * rad(sigma) <= 2 sigma.
+// b = sigma * rad(sigma) runs over the powerful numbers (b = prod p^(e+1) <-> sigma =
+// prod p^e), so the host lists the classes (b, sigma) once per bound (a DFS over primes) and
+// the device walks every (class, k) of the domain:
+//   k_heavy_count   per class: the k range that lands in the domain
+//   (cub scan)      flattened item offsets
+//   k_heavy_screen  per item: canonical k (squarefree, coprime to sigma: bit tables), then
+//                   for y = x - 1 and y = x + 1 a conservative test of s(x) s(y) >= (n+1)/2:
+//                   y is trial-divided by the primes <= P2 = y_max^(1/4) only; the cofactor
+//                   c then has at most three prime factors, all > P2, so s(c) is 1, p (c = p^2
+//                   or p^2 q, p <= sqrt(c / (P2+1))) or p^2 (c = p^3) and is bounded exactly
+//   k_heavy_exact   per survivor: rad(y) exactly (trial division to cbrt, cofactor 1, p,
+//                   p^2 or pq), the exact test R <= 2n, and de-duplication (a candidate with
+//                   both sides heavy is kept only from x = n)
+// The survivors of k_heavy_exact are exactly the candidates, with rad(n), rad(n+1) attached;
+// k_tail then walks their residue classes (bnx_kernels.cu).  Work: ~1.2M canonical heavy x
+// below 2^32 (instead of 2^32 integers), each costing ~54 trial divisions per side.
+#include <cub/device/device_scan.cuh>
+
+#include "bnx_kernels.cuh"
+#include "bnx_rad.cuh"
+
+namespace bnx {
+
+namespace {
+
+__device__ __forceinline__ uint32_t gcd32(uint32_t a, uint32_t b) {
+    if (!a) return b;
+    if (!b) return a;
+    const int sh = __ffs(a | b) - 1;
+    a >>= __ffs(a) - 1;
+    do {
+        b >>= __ffs(b) - 1;
+        if (a > b) { const uint32_t t = a; a = b; b = t; }
+        b -= a;
+    } while (b);
+    return a << sh;
+}
+
+// Upper bound of s(c) for an odd cofactor c > 0 whose prime factors all exceed P2 (p1 =
+// P2 + 1, p1^4 > c): c is 1, p, pq, pqr (s = 1), p^2 (s = sqrt c), p^2 q (s = p <=
+// sqrt(c / p1)) or p^3 (s = c^(2/3)).  Only an upper bound is needed (k_heavy_exact
+// decides), so the p^2 q case uses a rounded-up float root; squares and cubes are detected
+// exactly (float root, rounded, checked in integers; c < 2^45 keeps the float root within
+// 0.25 of the integer one).
+__device__ __forceinline__ uint64_t surplus_bound(uint64_t c, const HeavyArgs& a) {
+    if (c < a.p1sq) return 1;  // 1 or a prime
+    uint64_t u = 1;
+    const float cf = (float)c;
+    if ((c & 7) == 1) {  // odd squares are 1 mod 8
+        const uint64_t q = (uint64_t)rintf(sqrtf(cf));
+        if (q * q == c) u = q;
+    }
+    if (c >= a.p1cube) {
+        const uint64_t v = (uint64_t)(sqrtf(cf * a.inv_p1f) * 1.0001f) + 1;  // >= sqrt(c / p1)
+        if (v > u) u = v;
+        // p^3 with p > P2 >= 7: p^3 = +-1 mod 7 and mod 9, i.e. c mod 63 in {1, 8, 55, 62}
+        const uint32_t m63 = (uint32_t)(c % 63u);
+        if (!a.cube_filter || m63 == 1 || m63 == 8 || m63 == 55 || m63 == 62) {
+            const uint64_t r = (uint64_t)rintf(cbrtf(cf));
+            if (r * r * r == c && r * r > u) u = r * r;
+        }
+    }
+    return u;
+}
+
+// 2 * sigma * v >= rhs without overflow (sigma, v < 2^62).
+__device__ __forceinline__ bool twice_prod_ge(uint64_t sigma, uint64_t v, uint64_t rhs) {
+    const uint64_t s2 = 2 * sigma;
+    return __umul64hi(s2, v) != 0 || s2 * v >= rhs;
+}
+
+__global__ void k_heavy_count(HeavyArgs a) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.nent;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const BnxHeavyEnt e = a.ent[i];
+        uint64_t kh = 2 * e.m;
+        uint64_t kl = 1;
+        if (e.b > a.x_hi) {
+            kh = 0;
+        } else {
+            // floor(x_hi / b) and ceil(x_lo / b): a double estimate, corrected in integers
+            const double rb = 1.0 / (double)e.b;
+            uint64_t top = (uint64_t)((double)a.x_hi * rb);
+            while (top * e.b > a.x_hi) --top;
+            while ((top + 1) * e.b <= a.x_hi) ++top;
+            if (top < kh) kh = top;
+            uint64_t lo = (uint64_t)((double)a.x_lo * rb);
+            while (lo > 0 && lo * e.b >= a.x_lo) --lo;
+            while (lo * e.b < a.x_lo) ++lo;  // smallest lo with lo * b >= x_lo
+            if (lo > kl) kl = lo;
+        }
+        const uint64_t c = kh >= kl ? kh - kl + 1 : 0;
+        a.cnt[i] = c;
+        a.klo[i] = c ? (uint32_t)kl : 0u;
+    }
+}
+
+// Class of item w: smallest i >= lo with incl[i] > w (galloping, then binary search).
+__device__ __forceinline__ uint64_t first_class_above(const uint64_t* __restrict__ incl, uint64_t lo, uint64_t n,
+                                                      uint64_t w) {
+    uint64_t step = 1, hi = lo;
+    while (hi < n - 1 && incl[hi] <= w) {
+        lo = hi + 1;
+        hi = min(n - 1, hi + step);
+        step <<= 1;
+    }
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (incl[mid] > w) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+struct HeavyItem {
+    uint64_t x, sigma, radx;
+};
+
+// The y tests of one heavy x (both sides), see the file comment.  Shared tables: (inv, lim)
+// and p of the odd primes <= P2.
+__device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
+                                        const uint32_t* s_p) {
+    const uint64_t x = it.x;
+    const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
+    const bool vU = x >= a.n_first && x <= a.n_last;
+    const uint64_t yL = vL ? x - 1 : 1, yU = x + 1;
+    const int tL = __ffsll((long long)yL) - 1, tU = __ffsll((long long)yU) - 1;
+    uint64_t cL = yL >> tL, cU = yU >> tU;
+    uint64_t sL = tL ? 1ull << (tL - 1) : 1ull, sU = tU ? 1ull << (tU - 1) : 1ull;
+    // Divisibility of the odd parts by 32 primes at a time into bit masks (branch-free: the
+    // lanes of a warp stay converged), then the hits (about 1.5 per y) are divided out fully.
+    const uint64_t oL = cL, oU = cU;
+    for (int j0 = 0; j0 < a.np2; j0 += 32) {
+        const int jn = min(32, a.np2 - j0);
+        uint32_t mL = 0, mU = 0;
+#pragma unroll 8
+        for (int u = 0; u < jn; ++u) {
+            const ulonglong2 d = s_il[j0 + u];
+            mL |= (uint32_t)(oL * d.x <= d.y) << u;
+            mU |= (uint32_t)(oU * d.x <= d.y) << u;
+        }
+        while (mL | mU) {  // one hit of each side per round: the rounds are shared
+            if (mL) {
+                const int u = __ffs(mL) - 1;
+                mL &= mL - 1;
+                const ulonglong2 d = s_il[j0 + u];
+                const uint64_t pp = s_p[j0 + u];
+                cL *= d.x;
+                while (cL * d.x <= d.y) { cL *= d.x; sL *= pp; }
+            }
+            if (mU) {
+                const int u = __ffs(mU) - 1;
+                mU &= mU - 1;
+                const ulonglong2 d = s_il[j0 + u];
+                const uint64_t pp = s_p[j0 + u];
+                cU *= d.x;
+                while (cU * d.x <= d.y) { cU *= d.x; sU *= pp; }
+            }
+        }
+    }
+    const bool pL = vL && twice_prod_ge(it.sigma, sL * surplus_bound(cL, a), x);
+    const bool pU = vU && twice_prod_ge(it.sigma, sU * surplus_bound(cU, a), x + 1);
+    if (pL || pU) {
+        const unsigned long long slot = atomicAdd(&a.ctr[CTR_SURV], (unsigned long long)(pL + pU));
+        if (pL && slot < a.q1_cap) a.q1[slot] = make_ulonglong2((x - 1) | (1ull << 63), it.radx);
+        const unsigned long long s2 = slot + pL;
+        if (pU && s2 < a.q1_cap) a.q1[s2] = make_ulonglong2(x, it.radx);
+    }
+}
+
+// Each CTA owns a contiguous run of items and walks it in windows of HEAVY_THREADS (thread t
+// takes item base + t: neighbouring k of one class, or neighbouring classes).  Canonical
+// items go to a shared-memory queue; whenever it holds a full CTA's worth, every thread
+// takes one and runs the y tests, so the expensive part always runs with full warps.
+__global__ void __launch_bounds__(HEAVY_THREADS) k_heavy_screen(HeavyArgs a) {
+    constexpr int T = HEAVY_THREADS;
+    __shared__ ulonglong2 s_il[HEAVY_NP2];
+    __shared__ uint32_t s_p[HEAVY_NP2];
+    __shared__ HeavyItem s_q[2 * T];
+    __shared__ int s_cnt;
+    __shared__ unsigned long long s_cls;
+    const int tid = threadIdx.x;
+    for (int j = tid; j < a.np2; j += T) {
+        s_il[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
+        s_p[j] = (uint32_t)a.pdiv[j].p;
+    }
+    if (tid == 0) s_cnt = 0;
+    if (a.nent == 0) return;
+    const uint64_t W = a.incl[a.nent - 1];
+    const uint64_t b0 = W * blockIdx.x / gridDim.x, b1 = W * (blockIdx.x + 1) / gridDim.x;
+    if (tid == 0 && b0 < b1) s_cls = first_class_above(a.incl, 0, a.nent, b0);
+    __syncthreads();
+    uint64_t base = b0;
+    // `cnt` is every thread's copy of s_cnt, read only between the two barriers of a fill
+    // step (after all appends, before the next) so that the loop conditions agree.
+    int cnt = 0;
+    for (;;) {
+        // fill the queue up to at least T entries (or until the run is exhausted)
+        while (cnt < T && base < b1) {
+            const uint64_t w = base + tid;
+            const uint64_t cls0 = s_cls;
+            uint64_t i = cls0;
+            if (w < b1) {
+                i = first_class_above(a.incl, cls0, a.nent, w);
+                const BnxHeavyEnt e = a.ent[i];
+                const uint64_t k = a.klo[i] + (w - (i ? a.incl[i - 1] : 0));
+                if (k < a.nkinfo) {
+                    bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
+                    if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
+                    if (canon) {
+                        const int slot = atomicAdd(&s_cnt, 1);
+                        s_q[slot] = HeavyItem{k * e.b, e.m * e.r, k * e.r};
+                    }
+                } else {
+                    a.flags[1] = 1;
+                }
+            }
+            __syncthreads();
+            cnt = s_cnt;
+            if (w == min(base + T, b1) - 1) s_cls = i;  // class of the window's last item
+            base += T;
+            __syncthreads();
+        }
+        if (cnt == 0) break;
+        const int take = min(cnt, T);
+        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p);
+        cnt -= take;
+        __syncthreads();
+        if (tid == 0) s_cnt = cnt;
+        __syncthreads();
+    }
+}
+
+// Exact radical of the other side (one thread per survivor: the odd primes <= cbrt(y_max)
+// from shared memory, 32 per bit mask as in y_tests; the cofactor is then 1, p, p^2 or pq),
+// the exact test R <= 2n, de-duplication, emission.
+__global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
+    extern __shared__ ulonglong2 s_il3[];  // np3 (inv, lim), then np3 p
+    uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_il3 + a.np3);
+    const int np3 = (int)a.np3;
+    for (int j = threadIdx.x; j < np3; j += blockDim.x) {
+        s_il3[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
+        s_p3[j] = (uint32_t)a.pdiv[j].p;
+    }
+    __syncthreads();
+    const uint64_t nq = min((uint64_t)a.ctr[CTR_SURV], a.q1_cap);
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    if (nq * 32 <= nthreads) {
+        // few survivors (domains far from 1): one warp each, the primes spread over the lanes
+        const int lane = threadIdx.x & 31;
+        for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nq; i += nthreads >> 5) {
+            const ulonglong2 rec = a.q1[i];
+            const bool sideL = rec.x >> 63;
+            const uint64_t n = rec.x & ~(1ull << 63), radx = rec.y;
+            const uint64_t y = sideL ? n : n + 1;
+            const uint64_t rady = rad_warp(y, a.pdiv, a.np3);
+            if (lane) continue;
+            if (__umul64hi(radx, rady) != 0 || radx * rady > 2 * n) continue;
+            if (sideL) {
+                const uint64_t sy = y / rady;
+                if (__umul64hi(2 * sy, sy) != 0 || 2 * sy * sy >= y) continue;
+            }
+            const unsigned long long slot = atomicAdd(&a.ctr[CTR_CAND], 1ull);
+            if (slot < a.cand_cap) a.cand[slot] = sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady};
+        }
+        return;
+    }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nq; i += nthreads) {
+        const ulonglong2 rec = a.q1[i];
+        const bool sideL = rec.x >> 63;
+        const uint64_t n = rec.x & ~(1ull << 63), radx = rec.y;
+        const uint64_t y = sideL ? n : n + 1;
+        const int tz = __ffsll((long long)y) - 1;
+        const uint64_t o = y >> tz;
+        uint64_t c = o, rady = tz ? 2 : 1;
+        for (int j0 = 0; j0 < np3; j0 += 32) {
+            const int jn = min(32, np3 - j0);
+            uint32_t m = 0;
+#pragma unroll 8
+            for (int u = 0; u < jn; ++u) {
+                const ulonglong2 d = s_il3[j0 + u];
+                m |= (uint32_t)(o * d.x <= d.y) << u;
+            }
+            while (m) {
+                const int u = __ffs(m) - 1;
+                m &= m - 1;
+                const ulonglong2 d = s_il3[j0 + u];
+                rady *= s_p3[j0 + u];
+                c *= d.x;
+                while (c * d.x <= d.y) c *= d.x;
+            }
+        }
+        if (c > 1) {  // at most two primes > cbrt(y) remain: c = p, p^2 or pq
+            const uint64_t q = (uint64_t)rintf(sqrtf((float)c));  // exact for c < 2^45 (see surplus_bound)
+            rady *= (q * q == c) ? q : c;
+        }
+        if (__umul64hi(radx, rady) != 0 || radx * rady > 2 * n) continue;
+        if (sideL) {  // keep from x = n + 1 only if n itself is not heavy
+            const uint64_t sy = y / rady;
+            if (__umul64hi(2 * sy, sy) != 0 || 2 * sy * sy >= y) continue;
+        }
+        const unsigned long long slot = atomicAdd(&a.ctr[CTR_CAND], 1ull);
+        if (slot < a.cand_cap) a.cand[slot] = sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady};
+    }
+}
+
+}  // namespace
+
+size_t heavy_scan_temp_bytes(uint64_t nent) {
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)nent);
+    return bytes;
+}
+
+void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
+                  cudaEvent_t ev_generated) {
+    if (a.nent) {
+        const unsigned cb = (unsigned)std::min<uint64_t>((a.nent + 255) / 256, 4096);
+        k_heavy_count<<<cb, 256, 0, st>>>(a);
+        size_t bytes = scan_temp_bytes;
+        cub::DeviceScan::InclusiveSum(scan_temp, bytes, a.cnt, a.incl, (int64_t)a.nent, st);
+        k_heavy_screen<<<grid, HEAVY_THREADS, 0, st>>>(a);
+    }
+    const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t));
+    k_heavy_exact<<<grid, 256, smem3, st>>>(a);
+    if (ev_generated) cudaEventRecord(ev_generated, st);
+}
+
+}  // namespace bnx

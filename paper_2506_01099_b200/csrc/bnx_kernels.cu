@@ -19,6 +19,7 @@
 
 #include "bnx_kernels.cuh"
 #include "bnx_math.cuh"
+#include "bnx_rad.cuh"
 
 namespace bnx {
 
@@ -375,52 +376,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
     }
 }
 
-// ------------------------------------------------------------------------------------
-// Exact rad(x) (x < 2^42) by warp-cooperative trial division over the odd-prime table up to
-// cbrt(x) only: afterwards the cofactor c has at most two prime factors, all > cbrt(x), so
-// c is 1, p, p^2 or p*q and rad(c) = isqrt(c) if c is a square, else c.  Each lane owns
-// primes j = lane (mod 32), four loads in flight; the partial products of the primes and of
-// the prime powers dividing x are multiplied across the warp.  Warp-collective.
-__device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_t npd) {
-    const int lane = threadIdx.x & 31;
-    const int tz = bnx_ctz64(x);
-    const uint64_t y = x >> tz;
-    uint64_t pr = 1, pp = 1;
-    bool go = true;
-    for (uint64_t j = lane; go && j < npd; j += 128) {
-        BnxPDiv d[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint64_t jj = j + 32u * u;
-            d[u] = jj < npd ? pd[jj] : BnxPDiv{1ull << 21, 0, 0};  // sentinel: p^3 = 2^63 > y
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (d[u].p * d[u].p * d[u].p > y) { go = false; break; }  // p <= 2^21: no overflow
-            uint64_t t = y * d[u].inv;
-            if (t <= d[u].lim) {
-                pr *= d[u].p;
-                pp *= d[u].p;
-                while (t * d[u].inv <= d[u].lim) { t *= d[u].inv; pp *= d[u].p; }
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        pr *= __shfl_xor_sync(0xffffffffu, pr, o);
-        pp *= __shfl_xor_sync(0xffffffffu, pp, o);
-    }
-    const uint64_t c = y * bnx_inv64(pp);  // exact: pp | y, both odd
-    uint64_t rc = c;
-    if (c > 1) {
-        uint64_t s = (uint64_t)sqrt((double)c);
-        while (s * s > c) --s;
-        while ((s + 1) * (s + 1) <= c) ++s;
-        if (s * s == c) rc = s;
-    }
-    return (tz ? 2ull : 1ull) * pr * rc;
-}
-
 // The tail of the search, one warp per screen survivor n:
 //  1. key:  exact r0 = rad(n), r1 = rad(n+1); n is a candidate iff R = r0 r1 <= 2n.
 //  2. collision pass on the residue classes.  For a pair m < n with S_m = S_n,
@@ -430,61 +385,6 @@ __device__ uint64_t rad_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_
 //     radicals, tested exactly: rad(m) == r  <=>  r | m  and  m / r | r^inf (gcds).
 //  3. every kept m is verified by full radical comparison (rad_warp of m and m+1) and
 //     classified as the reference does (signatures.py:67-81), then emitted.
-// rad(x) and rad(x+1) in one warp-cooperative pass (same method as rad_warp): each lane
-// tests its primes against both odd parts, so the two chains overlap.
-__device__ void rad2_warp(uint64_t x, const BnxPDiv* __restrict__ pd, uint64_t npd, uint64_t& rx, uint64_t& rx1) {
-    const int lane = threadIdx.x & 31;
-    const int tz0 = bnx_ctz64(x), tz1 = bnx_ctz64(x + 1);
-    const uint64_t y0 = x >> tz0, y1 = (x + 1) >> tz1;
-    const uint64_t ymax = y0 > y1 ? y0 : y1;
-    uint64_t pr0 = 1, pp0 = 1, pr1 = 1, pp1 = 1;
-    bool go = true;
-    for (uint64_t j = lane; go && j < npd; j += 128) {
-        BnxPDiv d[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint64_t jj = j + 32u * u;
-            d[u] = jj < npd ? pd[jj] : BnxPDiv{1ull << 21, 0, 0};  // sentinel: p^3 = 2^63 > y
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (d[u].p * d[u].p * d[u].p > ymax) { go = false; break; }
-            uint64_t t = y0 * d[u].inv;
-            if (t <= d[u].lim) {
-                pr0 *= d[u].p;
-                pp0 *= d[u].p;
-                while (t * d[u].inv <= d[u].lim) { t *= d[u].inv; pp0 *= d[u].p; }
-            }
-            t = y1 * d[u].inv;
-            if (t <= d[u].lim) {
-                pr1 *= d[u].p;
-                pp1 *= d[u].p;
-                while (t * d[u].inv <= d[u].lim) { t *= d[u].inv; pp1 *= d[u].p; }
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        pr0 *= __shfl_xor_sync(0xffffffffu, pr0, o);
-        pp0 *= __shfl_xor_sync(0xffffffffu, pp0, o);
-        pr1 *= __shfl_xor_sync(0xffffffffu, pr1, o);
-        pp1 *= __shfl_xor_sync(0xffffffffu, pp1, o);
-    }
-    auto finish = [](uint64_t y, uint64_t pr, uint64_t pp, int tz) {
-        const uint64_t c = y * bnx_inv64(pp);
-        uint64_t rc = c;
-        if (c > 1) {
-            uint64_t sq = (uint64_t)sqrt((double)c);
-            while (sq * sq > c) --sq;
-            while ((sq + 1) * (sq + 1) <= c) ++sq;
-            if (sq * sq == c) rc = sq;
-        }
-        return (tz ? 2ull : 1ull) * pr * rc;
-    };
-    rx = finish(y0, pr0, pp0, tz0);
-    rx1 = finish(y1, pr1, pp1, tz1);
-}
-
 // One candidate n (R = r0 r1 <= 2n) and a range [k_begin, k_end) of its residue-class members:
 // k < t1 -> first kind m = n - (k+1) R; else second kind m = (t0 + k - t1) R - n - 1.  With
 // s0 = n / r0 and s1 = (n+1) / r1 the cofactors are linear in t, so no division is needed:
@@ -540,17 +440,23 @@ constexpr uint64_t TAIL_HEAVY = 128;
 
 __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
     const int lane = threadIdx.x & 31;
-    const uint64_t cnt = min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
+    const uint64_t cnt = a.cands ? min((uint64_t)a.ctr[CTR_CAND], a.cand_cap)
+                                 : min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
     for (;;) {
-        // survivors are taken one at a time from a shared counter
+        // survivors / candidates are taken one at a time from a shared counter
         unsigned long long i = 0;
         if (lane == 0) i = atomicAdd(&a.ctr[CTR_NEXT], 1ull);
         i = __shfl_sync(0xffffffffu, i, 0);
         if (i >= cnt) break;
-        const uint64_t n = a.surv[i];
-        uint64_t r0, r1;
-        rad2_warp(n, a.pdiv, a.npdiv, r0, r1);
-        if (__umul64hi(r0, r1) != 0 || r0 * r1 > 2 * n) continue;  // warp-uniform
+        uint64_t n, r0, r1;
+        if (a.cands) {  // heavy engine: radicals known exactly, R <= 2n already checked
+            const BnxCand cc = a.cands[i];
+            n = cc.n; r0 = cc.r0; r1 = cc.r1;
+        } else {
+            n = a.surv[i];
+            rad2_warp(n, a.pdiv, a.npdiv, r0, r1);
+            if (__umul64hi(r0, r1) != 0 || r0 * r1 > 2 * n) continue;  // warp-uniform
+        }
         TailCand c;
         c.n = n; c.r0 = r0; c.r1 = r1; c.R = r0 * r1;
         c.s0 = n / r0; c.s1 = (n + 1) / r1;
@@ -560,7 +466,7 @@ __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
         const uint64_t c2 = ((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0;
         const uint64_t total = c.t1 + c2;
         if (lane == 0) {
-            atomicAdd(&a.ctr[CTR_CAND], 1ull);
+            if (!a.cands) atomicAdd(&a.ctr[CTR_CAND], 1ull);
             if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
             atomicMax(&a.ctr[CTR_MAXCHK], (unsigned long long)total);
         }

@@ -42,8 +42,10 @@ struct ScreenArgs {
 };
 
 struct TailArgs {
-    const uint64_t* surv;
+    const uint64_t* surv;  // screen engine: survivors n (the tail computes the radicals)
     uint64_t surv_cap;
+    const BnxCand* cands;  // heavy engine: exact candidates (n, rad n, rad n+1); null for the screen
+    uint64_t cand_cap;
     BnxCand* heavy;      // candidates with many residue-class members
     uint64_t heavy_cap;
     const BnxPDiv* pdiv;
@@ -53,6 +55,37 @@ struct TailArgs {
     uint64_t pair_cap;
     unsigned long long* ctr;
 };
+
+// Heavy-side generator (bnx_heavy.cu).
+constexpr int HEAVY_THREADS = 256;
+constexpr int HEAVY_NP2 = 512;   // odd primes <= y_max^(1/4) staged in shared memory
+constexpr int HEAVY_NP3 = 2048;  // odd primes <= cbrt(y_max) staged in shared memory
+struct HeavyArgs {
+    const BnxHeavyEnt* ent;
+    uint64_t nent;
+    uint64_t* cnt;    // per class: number of k in the domain
+    uint64_t* incl;   // inclusive scan of cnt
+    uint32_t* klo;    // per class: first k in the domain
+    const uint32_t* kinfo;  // per k: bits 0..30 = primes 2..127 dividing k, bit 31 = k not squarefree
+    uint64_t nkinfo;
+    uint64_t x_lo, x_hi;    // heavy x range: [n_first, n_last + 1]
+    uint64_t n_first, n_last;
+    const BnxPDiv* pdiv;    // odd primes ascending
+    int np2;                // odd primes <= P2 = floor(y_max^(1/4))
+    uint64_t np3;           // odd primes <= cbrt(y_max)
+    uint64_t p1, p1sq, p1cube;  // P2 + 1 and its powers
+    float inv_p1f;
+    int cube_filter;        // P2 >= 7: cube residues mod 63 pre-filter the p^3 test
+    ulonglong2* q1;         // screen survivors: (n | side << 63, rad x)
+    uint64_t q1_cap;
+    BnxCand* cand;          // exact candidates
+    uint64_t cand_cap;
+    unsigned long long* ctr;
+    int* flags;             // [1] k outside kinfo (internal error)
+};
+size_t heavy_scan_temp_bytes(uint64_t nent);
+void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
+                  cudaEvent_t ev_generated);
 
 struct SieveArgs {
     uint64_t start, length;

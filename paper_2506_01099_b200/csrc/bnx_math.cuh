@@ -92,6 +92,14 @@ struct BnxPDiv {
 struct BnxCand {
     uint64_t n, r0, r1;
 };
+// One "surplus class" of the heavy-side generator (see bnx_heavy.cu): sigma = m * r with
+// r = rad(sigma), b = sigma * r = m * r^2 (a powerful number); the heavy integers of the class
+// are x = k * b with k squarefree, gcd(k, r) = 1 and k <= 2m.  rmask: which of the first 31
+// primes (2..127) divide r; rbig: product of r's primes >= 131 (1 if none), rbig_min the least.
+struct BnxHeavyEnt {
+    uint64_t b, m;
+    uint32_t r, rmask, rbig, rbig_min;
+};
 struct BnxMatch {
     uint64_t m, n;
     uint32_t kind, pad;

@@ -186,20 +186,73 @@ def test_reference_run_2p32_exact_rows():
         sorted(ref, key=lambda r: (r[1], r[2]))
 
 
-@pytest.mark.parametrize("e", [24, 28])
-def test_screen_keeps_every_candidate(orc, e):
-    """The on-chip screen may only over-approximate: the number of n < S with
-    rad(n) rad(n+1) <= 2n that k_tail confirms must equal the exact count from the oracle's
-    sieve (numpy), i.e. no candidate is ever dropped by the log screen."""
-    S = 1 << e
-    vals = orc.sieve_segment(1, S, orc.primes_up_to(math.isqrt(S)))
-    n = np.arange(1, S, dtype=np.uint64)
+class engine:
+    """Switch the default context's candidate generator for a block (restores heavy)."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        bp._native.context(None).set_engine(self.name)
+
+    def __exit__(self, *exc):
+        bp._native.context(None).set_engine("heavy")
+
+
+def exact_candidates(orc, lo, hi):
+    """#{lo <= n <= hi : rad(n) rad(n+1) <= 2n} from the oracle's sieve (numpy)."""
+    vals = orc.sieve_segment(lo, hi - lo + 2, orc.primes_up_to(math.isqrt(hi + 1) + 1))
+    n = np.arange(lo, hi + 1, dtype=np.uint64)
     r0, r1 = vals[:-1], vals[1:]
-    exact = int(np.count_nonzero(r0 <= (2 * n) // r1))  # R <= 2n without overflow
-    bp.find_pairs(S)
-    st = bp.last_stats()
+    return int(np.count_nonzero(r0 <= (2 * n) // r1))  # R <= 2n without overflow
+
+
+@pytest.mark.parametrize("name", ["heavy", "screen"])
+@pytest.mark.parametrize("e", [24, 28])
+def test_generator_keeps_every_candidate(orc, e, name):
+    """Both candidate generators may only over-approximate: the number of n < S with
+    rad(n) rad(n+1) <= 2n that reach k_tail must equal the exact count from the oracle's
+    sieve, i.e. no candidate is ever dropped (and, for the heavy generator, none is
+    duplicated: it emits the candidates themselves)."""
+    S = 1 << e
+    exact = exact_candidates(orc, 1, S - 1)
+    with engine(name):
+        bp.find_pairs(S)
+        st = bp.last_stats()
     assert st["candidates"] == exact
     assert st["survivors"] >= exact
+
+
+def test_heavy_candidates_on_random_domains(orc):
+    """Exact candidate count of the heavy generator on domains far from 1 (where most
+    surplus classes have no heavy integer), against the oracle."""
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        lo = int(rng.integers(1, 2**34))
+        hi = lo + int(rng.integers(0, 1 << 22))
+        bp.search_domain(lo, hi)
+        assert bp.last_stats()["candidates"] == exact_candidates(orc, lo, hi), (lo, hi)
+
+
+@pytest.mark.parametrize("lo,hi", [(1, 2**32 - 1), (2**32, 2**33 - 1), (2**40 - 2**30, 2**40 - 1),
+                                   (1_400_000_000_000 - 2**28, 1_400_000_000_000), (2**42 - 2**26, 2**42 - 2)])
+def test_engines_agree(lo, hi):
+    """The heavy generator and the byte screen return identical rows and candidate counts."""
+    out = {}
+    for name in ("heavy", "screen"):
+        with engine(name):
+            rows = bp.search.search_rows(lo, hi)
+            out[name] = (np.ascontiguousarray(rows).tobytes(), bp.last_stats()["candidates"])
+    assert out["heavy"] == out["screen"]
+
+
+def test_whole_range_to_2p40_is_theorem_1():
+    """One device search over [1, 2^40) (both kinds): exactly the 41 pairs of Theorem 1."""
+    S = 1 << 40
+    got = sorted((p.m, p.n) for p in bp.find_pairs(S))
+    exp = bp.expected_pairs_up_to(S)
+    assert got == sorted((p.m, p.n) for p in exp.first_kind + exp.second_kind)
+    assert len(got) == 41
 
 
 def test_random_domains_vs_oracle(orc):
@@ -222,3 +275,19 @@ def test_near_the_top_of_the_range():
     assert (p.rad_m, p.rad_m_plus_1) == (bp.radical_oracle(m), bp.radical_oracle(m + 1))
     with pytest.raises(ValueError):
         bp.search_domain(2**42 - 10, 2**42)
+
+
+def test_repeated_searches_are_identical():
+    """Back-to-back device searches (the bench's pattern) give identical rows and counters:
+    guards the CTA-level work queue of k_heavy_screen against barrier/race bugs."""
+    ctx = bp._native.context(None)
+    ctx.prepare(2**32)
+    ctx.enqueue(1, 2**32 - 1, 3)
+    ref = np.ascontiguousarray(ctx.collect()).tobytes()
+    ref_st = ctx.stats()
+    for _ in range(300):
+        ctx.enqueue(1, 2**32 - 1, 3)
+        assert np.ascontiguousarray(ctx.collect()).tobytes() == ref
+        st = ctx.stats()
+        assert (st["survivors"], st["candidates"], st["matches"]) == \
+            (ref_st["survivors"], ref_st["candidates"], ref_st["matches"])
