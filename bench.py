@@ -6,16 +6,18 @@ Workload (BASELINE.json configs[1]): first-kind search below S = 2^32 on one B20
 the search below S = N * 2^32 (weak scaling, no data-path collective).
 
   value     integers searched / s with the prime tables resident in HBM: per step one
-            device search (k_screen -> k_tail -> k_tail_heavy) timed with CUDA events
-            on the launching stream, L2 flushed (256 MiB write) before every step, max over
-            ranks.
+            device search (heavy generator: k_heavy_count -> cub scan -> k_heavy_screen ->
+            k_heavy_exact, then k_tail -> k_tail_heavy) timed with CUDA events on the
+            launching stream, L2 flushed (256 MiB write) before every step, max over ranks.
   e2e       the same metric through the public API (search_domain with a host PrimeList in
             pinned memory -> H2D copy, table build, search, D2H of the rows; for N > 1 plus
             the gather of all rows to every rank).
-  roofline  the dominant kernel (k_screen) against the HBM roofline of SURVEY.md section 8(d):
-            32 algorithmic bytes per integer searched (one 16-byte key record written and read),
-            timed live with CUDA events.  The screen keeps every per-integer quantity in
-            shared memory, so frac > 1 is expected; see DESIGN.md "Roofline".
+  roofline  the dominant stage (the candidate generator) against the HBM roofline of SURVEY.md
+            section 8(d): 32 algorithmic bytes per integer searched (one 16-byte key record
+            written and read), timed live with CUDA events.  The generator never touches a
+            per-integer record (it visits ~0.03% of the integers), so frac >> 1 is expected;
+            its own limiter, instruction issue, is reported beside it (issue_roofline, from
+            the ncu launch list in profiles/); see DESIGN.md "Roofline".
   cpu_baseline  the reference's chunked Algorithm 3 (oracle/oracle.c, a C restatement of
             chunked.py:307-412 at the reference defaults: chunk 2^27, all host threads) on a
             bounded sample (one chunk build + one parallel round of probes), extrapolated to
@@ -60,8 +62,9 @@ def load_peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic() -> dict | None:
-    path = os.path.join(ROOT, "profiles", "ncu_screen_traffic.json")
+def load_traffic(engine: str) -> dict | None:
+    name = "ncu_heavy_generator.json" if engine == "heavy" else "ncu_screen_traffic.json"
+    path = os.path.join(ROOT, "profiles", name)
     if os.path.exists(path):
         with open(path) as f:
             return json.load(f)
@@ -355,24 +358,49 @@ def run_ours(args) -> None:
     e2e_value = ints / (e2e_ms_max / 1e3)
     h2d = 8 * len(plist.primes)
 
+    # ---- the same step with the byte-screen engine (visits every integer; identical rows)
+    screen_engine = None
+    if rank == 0 and ctx.engine() == "heavy":
+        ctx.set_engine("screen")
+        ctx.prepare(hi + 1)
+        for _ in range(2):
+            ctx.enqueue(lo, hi, int(kinds))
+            ctx.collect()
+        sms = []
+        same = True
+        for k in range(5):
+            flush.fill_(k & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.enqueue(lo, hi, int(kinds))
+            b.record(stream)
+            rows_s = ctx.collect()
+            sms.append(a.elapsed_time(b))
+            same &= [(int(r["m"]), int(r["n"])) for r in rows_s] == exp_keys
+        ctx.set_engine("heavy")
+        screen_engine = {"engine": "screen (k_screen: one byte per integer, every integer visited)",
+                         "ms_per_step": sum(sms) / len(sms), "value": ints_local / (sum(sms) / len(sms) / 1e3),
+                         "unit": "n/s", "same_pairs": same}
+
     # ---- roofline of the dominant kernel ---------------------------------------------------
     peak, peak_src = load_peaks()
     scr_ms = sum(screen_ms) / len(screen_ms)
     achieved = BYTES_PER_INT * ints_local / (scr_ms / 1e3) / 1e9
-    traffic = load_traffic()
+    engine = ctx.engine()
+    traffic = load_traffic(engine)
     traffic_bytes = None
     issue = None
     if traffic and traffic.get("dram_bytes_per_integer") is not None:
         traffic_bytes = traffic["dram_bytes_per_integer"] * ints_local
     if traffic and traffic.get("warp_inst_per_integer"):
-        # the screen's own limiter: SM instruction issue (4 warp-instructions per SM per clock)
+        # the generator's own limiter: SM instruction issue (4 warp-instructions per SM per clock)
         props = torch.cuda.get_device_properties(dev)
         max_mhz = clocks.get("sm_max_mhz") or 1965.0
         peak_issue = props.multi_processor_count * 4 * max_mhz * 1e6
         ach_issue = traffic["warp_inst_per_integer"] * ints_local / (scr_ms / 1e3)
         issue = {"achieved": ach_issue, "peak": peak_issue, "unit": "warp-instructions/s",
                  "frac": ach_issue / peak_issue,
-                 "inst_per_integer_source": f"ncu {traffic.get('source')} ({traffic['warp_inst_per_integer']:.4f} warp-inst/int)"}
+                 "inst_per_integer_source": f"ncu {traffic.get('source')} ({traffic['warp_inst_per_integer']:.6f} warp-inst/int)"}
 
     # ---- secondary: the exact radical sieve (radical.py:109-124) materialising rad(x) as
     # uint64 in HBM -- a write-bound kernel, 8 algorithmic bytes per integer
@@ -458,16 +486,21 @@ def run_ours(args) -> None:
             "gpu_launches": stats["kernel_launches"] * args.steps,
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_bytes, "kernel": "k_screen",
-                "model": ("SURVEY.md 8(d): 32 B per integer (16-B record written + read); k_screen keeps all "
-                          "per-integer state in shared memory, so achieved/peak > 1 measures the traffic the "
-                          "record design would need and this design avoids (DESIGN.md 'Roofline')"),
+                "traffic": traffic_bytes,
+                "kernel": ("heavy generator: k_heavy_count + cub scan + k_heavy_screen + k_heavy_exact"
+                           if engine == "heavy" else "k_screen"),
+                "engine": engine,
+                "model": ("SURVEY.md 8(d): 32 B per integer (16-B record written + read); the generator keeps no "
+                          "per-integer state at all, so achieved/peak > 1 measures the traffic the record design "
+                          "would need and this design avoids; issue_roofline is its real limiter "
+                          "(DESIGN.md 'Roofline')"),
                 "peak_source": peak_src,
-                "screen_ms_per_launch": scr_ms,
+                "generator_ms_per_search": scr_ms,
                 "pipeline_ms_per_step": sum(pipe_ms) / len(pipe_ms),
-                "screen_share_of_step": scr_ms / ms_local,
+                "generator_share_of_step": scr_ms / ms_local,
                 "issue_roofline": issue,
             },
+            "screen_engine": screen_engine,
             "cpu_baseline": cpu,
             "sieve_roofline": sieve,
             "wall_to_2p40": wall40,

@@ -179,10 +179,10 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
 // takes item base + t: neighbouring k of one class, or neighbouring classes).  Canonical
 // items go to a shared-memory queue; whenever it holds a full CTA's worth, every thread
 // takes one and runs the y tests, so the expensive part always runs with full warps.
-__global__ void __launch_bounds__(HEAVY_THREADS) k_heavy_screen(HeavyArgs a) {
+__global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) {
     constexpr int T = HEAVY_THREADS;
-    __shared__ ulonglong2 s_il[HEAVY_NP2];
-    __shared__ uint32_t s_p[HEAVY_NP2];
+    extern __shared__ ulonglong2 s_il[];  // np2 (inv, lim), then np2 p
+    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + a.np2);
     __shared__ HeavyItem s_q[2 * T];
     __shared__ int s_cnt;
     __shared__ unsigned long long s_cls;
@@ -326,7 +326,8 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         k_heavy_count<<<cb, 256, 0, st>>>(a);
         size_t bytes = scan_temp_bytes;
         cub::DeviceScan::InclusiveSum(scan_temp, bytes, a.cnt, a.incl, (int64_t)a.nent, st);
-        k_heavy_screen<<<grid, HEAVY_THREADS, 0, st>>>(a);
+        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint32_t));
+        k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
     }
     const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t));
     k_heavy_exact<<<grid, 256, smem3, st>>>(a);

@@ -1,7 +1,7 @@
 """The B200 search engine: every Benelux pair with n in a domain, on one GPU.
 
-The whole path runs on the device (csrc/bnx_kernels.cu):
-  k_screen -> k_verify -> k_enumerate -> k_finalize
+The whole path runs on the device (csrc/bnx_heavy.cu, csrc/bnx_kernels.cu):
+  k_heavy_count -> scan -> k_heavy_screen -> k_heavy_exact -> k_tail -> k_tail_heavy
 and the host only receives the (tiny) verified pair list.  See DESIGN.md for the lemma
 (rad(n) rad(n+1) <= 2n for every pair) that lets the collision pass work per n without
 materialising any per-integer record.
