@@ -106,7 +106,11 @@ struct HeavyTab {
     DBuf<uint32_t> kinfo;
     uint64_t nkinfo = 0;
     DBuf<uint64_t> cnt, incl;
-    DBuf<uint32_t> klo;
+    DBuf<uint32_t> klo, kcnt;
+    DBuf<uint32_t> tasks;  // k_heavy_sieve marking tasks for (tasks_np2, tasks_kc)
+    DBuf<uint16_t> invtab;  // inverses mod p of the primes <= P2 (k_heavy_sieve)
+    DBuf<uint32_t> invoff;
+    int ntasks = 0, tasks_np2 = -1, tasks_kc = 0;
     DBuf<unsigned char> scan_temp;
     size_t scan_bytes = 0;
     std::vector<uint64_t> sigma;  // host mirror: sigma of each class, ascending
@@ -116,6 +120,11 @@ struct HeavyTab {
         cnt.release();
         incl.release();
         klo.release();
+        kcnt.release();
+        tasks.release();
+        invtab.release();
+        invoff.release();
+        tasks_np2 = -1;
         scan_temp.release();
         gen = ~0ull;
         max_x = 0;
@@ -144,6 +153,7 @@ struct bnx_ctx {
     Tables screen_tab, sieve_tab, td_tab;
     HeavyTab heavy_tab;
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
+    uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
     DBuf<ulonglong2> q1;
     DBuf<BnxCand> cand;
 
@@ -426,6 +436,7 @@ int build_heavy(bnx_ctx* c, uint64_t max_x) {
     TRY(h.cnt.ensure(ents.size()));
     TRY(h.incl.ensure(ents.size()));
     TRY(h.klo.ensure(ents.size()));
+    TRY(h.kcnt.ensure(ents.size()));
     h.scan_bytes = heavy_scan_temp_bytes(ents.size());
     TRY(h.scan_temp.ensure(h.scan_bytes));
     CK(cudaMemcpyAsync(h.ent.p, ents.data(), sizeof(BnxHeavyEnt) * ents.size(), cudaMemcpyHostToDevice, c->stream));
@@ -476,9 +487,53 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     const uint64_t np2 = std::min<uint64_t>(odd_upto(p2), t.npdiv), np3 = std::min<uint64_t>(odd_upto(p3), t.npdiv);
     if (np2 > (uint64_t)HEAVY_NP2 || np3 > (uint64_t)HEAVY_NP3)
         return fail(BNX_ERR_RANGE, "bound too large for the heavy generator");
+    // k_heavy_sieve: chunk length (masks of 32 primes per word, ~32 KB of shared memory) and
+    // the marking tasks: prime j, side, sub-progression r of R, about HEAVY_TASK_HITS hits each
+    const int W = (int)((np2 + 31) / 32);
+    const int kc = std::max(32, std::min(4096, (6144 / std::max(W, 1)) & ~31));
+    if (h.tasks_np2 != (int)np2 || h.tasks_kc != kc) {
+        std::vector<uint32_t> tk, ioff;
+        std::vector<uint16_t> itab;
+        for (uint64_t j = 0; j < np2; ++j) {
+            const uint32_t p = c->h_primes[j + (c->h_primes[0] == 2 ? 1 : 0)];
+            ioff.push_back((uint32_t)itab.size());
+            itab.push_back(0);
+            for (uint32_t v = 1; v < p; ++v) {  // v^-1 = v^(p-2) mod p
+                uint64_t r = 1, base = v, e = p - 2;
+                for (; e; e >>= 1, base = base * base % p)
+                    if (e & 1) r = r * base % p;
+                itab.push_back((uint16_t)r);
+            }
+            const uint32_t hits = (uint32_t)((kc + p - 1) / p);
+            const uint32_t R = std::max<uint32_t>(1, (hits + HEAVY_TASK_HITS - 1) / HEAVY_TASK_HITS);
+            for (uint32_t side = 0; side < 2; ++side)
+                for (uint32_t r = 0; r < R; ++r) tk.push_back((uint32_t)j | side << 10 | r << 11 | R << 21);
+        }
+        TRY(h.tasks.ensure(tk.size()));
+        TRY(h.invtab.ensure(itab.size()));
+        TRY(h.invoff.ensure(ioff.size() + 1));
+        CK(cudaMemcpyAsync(h.tasks.p, tk.data(), sizeof(uint32_t) * tk.size(), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(h.invtab.p, itab.data(), sizeof(uint16_t) * itab.size(), cudaMemcpyHostToDevice, c->stream));
+        if (!ioff.empty())
+            CK(cudaMemcpyAsync(h.invoff.p, ioff.data(), sizeof(uint32_t) * ioff.size(), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        h.ntasks = (int)tk.size();
+        h.tasks_np2 = (int)np2;
+        h.tasks_kc = kc;
+    }
     CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
     HeavyArgs ha{};
+    ha.kcnt = h.kcnt.p;
+    ha.tasks = h.tasks.p;
+    ha.ntasks = h.ntasks;
+    ha.kc = kc;
+    // measured (scripts/engine_compare.py, KMIN sweep): with <= 64 primes below P2 (bounds
+    // up to ~2^33) trial division is as fast as the sieve; above, sieving classes with >= 512
+    // k is best (2^40: 5.8 ms vs 8.3 ms)
+    ha.kmin = c->heavy_kmin ? c->heavy_kmin : (np2 <= 64 ? ~0ull : HEAVY_KMIN_DEFAULT);
+    ha.invtab = h.invtab.p;
+    ha.invoff = h.invoff.p;
     // first class with 2 sigma^2 >= n_first (smaller sigma have no heavy x in the domain)
     const uint64_t smin = isqrt_u64(n_first / 2);
     const uint64_t start = (uint64_t)(std::lower_bound(h.sigma.begin(), h.sigma.end(), smin) - h.sigma.begin());
@@ -522,7 +577,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     c->q_kinds = kinds;
     c->stats = bnx_stats_t{};
     c->stats.integers = n_last - n_first + 1;
-    c->stats.kernel_launches = ha.nent ? 7 : 3;  // count, scan (2), screen, exact, tail, tail_heavy
+    // count, scan (2), screen, [sieve], exact, tail, tail_heavy
+    c->stats.kernel_launches = ha.nent ? (ha.kmin != ~0ull ? 8 : 7) : 3;
     return BNX_OK;
 }
 
@@ -658,6 +714,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
+    if (const char* env = std::getenv("BNX_HEAVY_KMIN")) c->heavy_kmin = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
         const int v = std::atoi(env);
         if (v >= 0 && v < screen_variant_count()) c->screen_v = v;

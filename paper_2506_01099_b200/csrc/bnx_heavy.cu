@@ -98,8 +98,9 @@ __global__ void k_heavy_count(HeavyArgs a) {
             if (lo > kl) kl = lo;
         }
         const uint64_t c = kh >= kl ? kh - kl + 1 : 0;
-        a.cnt[i] = c;
+        a.cnt[i] = c >= a.kmin ? ((c + a.kc - 1) / a.kc) << 40 : c;  // sieve chunks | trial items
         a.klo[i] = c ? (uint32_t)kl : 0u;
+        a.kcnt[i] = (uint32_t)c;
     }
 }
 
@@ -107,14 +108,14 @@ __global__ void k_heavy_count(HeavyArgs a) {
 __device__ __forceinline__ uint64_t first_class_above(const uint64_t* __restrict__ incl, uint64_t lo, uint64_t n,
                                                       uint64_t w) {
     uint64_t step = 1, hi = lo;
-    while (hi < n - 1 && incl[hi] <= w) {
+    while (hi < n - 1 && (incl[hi] & HEAVY_TRIAL_MASK) <= w) {
         lo = hi + 1;
         hi = min(n - 1, hi + step);
         step <<= 1;
     }
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
-        if (incl[mid] > w) hi = mid; else lo = mid + 1;
+        if ((incl[mid] & HEAVY_TRIAL_MASK) > w) hi = mid; else lo = mid + 1;
     }
     return lo;
 }
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) 
     }
     if (tid == 0) s_cnt = 0;
     if (a.nent == 0) return;
-    const uint64_t W = a.incl[a.nent - 1];
+    const uint64_t W = a.incl[a.nent - 1] & HEAVY_TRIAL_MASK;
     const uint64_t b0 = W * blockIdx.x / gridDim.x, b1 = W * (blockIdx.x + 1) / gridDim.x;
     if (tid == 0 && b0 < b1) s_cls = first_class_above(a.incl, 0, a.nent, b0);
     __syncthreads();
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) 
             if (w < b1) {
                 i = first_class_above(a.incl, cls0, a.nent, w);
                 const BnxHeavyEnt e = a.ent[i];
-                const uint64_t k = a.klo[i] + (w - (i ? a.incl[i - 1] : 0));
+                const uint64_t k = a.klo[i] + (w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0));
                 if (k < a.nkinfo) {
                     bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
                     if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
@@ -235,6 +236,174 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) 
         __syncthreads();
         if (tid == 0) s_cnt = cnt;
         __syncthreads();
+    }
+}
+
+// Inverse of a modulo p (0 < a < p, p prime), extended Euclid in 32 bits.
+__device__ __forceinline__ uint32_t inv_mod_u32(uint32_t a, uint32_t p) {
+    int32_t t = 0, nt = 1;
+    uint32_t r = p, nr = a;
+    while (nr) {
+        const uint32_t q = r / nr;
+        const int32_t tt = t - (int32_t)q * nt;
+        t = nt;
+        nt = tt;
+        const uint32_t rr = r - q * nr;
+        r = nr;
+        nr = rr;
+    }
+    return (uint32_t)(t < 0 ? t + (int32_t)p : t);
+}
+
+// Classes with many k: y = k b -+ 1 runs through an arithmetic progression in k, so for an
+// odd prime p not dividing b, p | k b + 1 <=> k = -b^-1 and p | k b - 1 <=> k = +b^-1 (mod p).
+// Each CTA owns a contiguous run of chunks (up to kc consecutive k of one class each):
+//   1. per prime <= P2, on entering a class: b mod p (Barrett with the table's
+//      floor((2^64-1)/p)), b^-1 mod p (host table), the first index of each side's
+//      progression in the chunk; for the next chunk of the same class the indices just
+//      move by kc mod p;
+//   2. marks: host-built tasks of ~16 hits each set bit j of word j/32 of the k's mask
+//      (shared atomicOr; one mask per side and 32 primes);
+//   3. canonical k of the chunk are compacted into a shared list;
+//   4. per canonical k: the marked primes are divided out of both y exactly (with their
+//      powers) and the same stage-1 test as k_heavy_screen decides.
+// So the per-k work is ~3 marks and ~3 exact divisions instead of 2 pi(P2) trial divisions.
+__device__ __forceinline__ uint64_t mod_by_lim(uint64_t v, uint64_t p, uint64_t lim) {
+    uint64_t r = v - __umul64hi(v, lim) * p;  // lim = floor((2^64-1)/p): quotient off by <= 1
+    while (r >= p) r -= p;
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int np2 = a.np2, kc = a.kc, W = (np2 + 31) >> 5;
+    uint32_t* masks = reinterpret_cast<uint32_t*>(sm_raw);               // [2][W][kc]
+    ulonglong2* s_il = reinterpret_cast<ulonglong2*>(masks + 2 * W * kc);  // np2
+    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + np2);                // np2
+    int32_t* s_off = reinterpret_cast<int32_t*>(s_p + np2);                 // 2 np2
+    uint32_t* s_kcm = reinterpret_cast<uint32_t*>(s_off + 2 * np2);         // np2: kc mod p
+    uint32_t* s_task = s_kcm + np2;                                         // ntasks
+    uint32_t* s_list = s_task + a.ntasks;                                   // kc
+    __shared__ BnxHeavyEnt s_e;
+    __shared__ uint64_t s_k0, s_kend, s_cls_end;
+    __shared__ int s_nl, s_fresh;
+    const int tid = threadIdx.x;
+    for (int j = tid; j < np2; j += blockDim.x) {
+        s_il[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
+        s_p[j] = (uint32_t)a.pdiv[j].p;
+        s_kcm[j] = (uint32_t)kc % (uint32_t)a.pdiv[j].p;
+    }
+    for (int t = tid; t < a.ntasks; t += blockDim.x) s_task[t] = a.tasks[t];
+    if (a.nent == 0) return;
+    const uint64_t C = a.incl[a.nent - 1] >> 40;
+    const uint64_t c_begin = C * blockIdx.x / gridDim.x, c_end = C * (blockIdx.x + 1) / gridDim.x;
+    for (uint64_t ch = c_begin; ch < c_end; ++ch) {
+        __syncthreads();
+        if (tid == 0) {
+            if (ch == c_begin || ch >= s_cls_end) {  // entering a class
+                uint64_t lo = 0, hi = a.nent - 1;      // first class with chunk prefix > ch
+                while (lo < hi) {
+                    const uint64_t mid = (lo + hi) >> 1;
+                    if ((a.incl[mid] >> 40) > ch) hi = mid; else lo = mid + 1;
+                }
+                const uint64_t first = lo ? a.incl[lo - 1] >> 40 : 0;
+                s_e = a.ent[lo];
+                s_k0 = (uint64_t)a.klo[lo] + (ch - first) * (uint64_t)kc;
+                s_kend = (uint64_t)a.klo[lo] + a.kcnt[lo];
+                s_cls_end = a.incl[lo] >> 40;
+                s_fresh = 1;
+            } else {
+                s_k0 += (uint64_t)kc;
+                s_fresh = 0;
+            }
+            s_nl = 0;
+        }
+        __syncthreads();
+        const BnxHeavyEnt e = s_e;
+        const uint64_t k0 = s_k0;
+        const int kn = (int)min((uint64_t)kc, s_kend - k0);
+        const bool fresh = s_fresh;
+        // 1. progressions (full set-up on entering a class, else shifted by kc)
+        for (int j = tid; j < np2; j += blockDim.x) {
+            const uint32_t p = s_p[j];
+            if (fresh) {
+                const uint64_t lim = s_il[j].y;
+                const uint32_t bm = (uint32_t)mod_by_lim(e.b, p, lim);
+                if (bm == 0) {
+                    s_off[2 * j] = s_off[2 * j + 1] = -1;
+                } else {
+                    const uint32_t inv = a.invtab[a.invoff[j] + bm];
+                    const uint32_t k0m = (uint32_t)mod_by_lim(k0, p, lim);
+                    s_off[2 * j] = (int32_t)((2 * p - inv - k0m) % p);  // k = -b^-1: p | k b + 1
+                    s_off[2 * j + 1] = (int32_t)((inv + p - k0m) % p);  // k = +b^-1: p | k b - 1
+                }
+            } else if (s_off[2 * j] >= 0) {
+                const uint32_t d = p - s_kcm[j];
+                s_off[2 * j] = (int32_t)(((uint32_t)s_off[2 * j] + d) % p);
+                s_off[2 * j + 1] = (int32_t)(((uint32_t)s_off[2 * j + 1] + d) % p);
+            }
+        }
+        for (int w = tid; w < (2 * W * kc) >> 2; w += blockDim.x) reinterpret_cast<uint4*>(masks)[w] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        // 2. marks
+        for (int t = tid; t < a.ntasks; t += blockDim.x) {
+            const uint32_t tk = s_task[t];
+            const int j = tk & 0x3FF, side = (tk >> 10) & 1;
+            const uint32_t r = (tk >> 11) & 0x3FF, R = tk >> 21;
+            const int32_t off = s_off[2 * j + side];
+            if (off < 0) continue;
+            const uint32_t p = s_p[j];
+            uint32_t* m = masks + (side * W + (j >> 5)) * kc;
+            const uint32_t bit = 1u << (j & 31);
+            for (uint32_t kk = (uint32_t)off + r * p; kk < (uint32_t)kn; kk += R * p) atomicOr(&m[kk], bit);
+        }
+        // 3. canonical k of the chunk
+        for (int kk = tid; kk < kn; kk += blockDim.x) {
+            const uint64_t k = k0 + kk;
+            if (k >= a.nkinfo) { a.flags[1] = 1; continue; }
+            bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
+            if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
+            if (canon) s_list[atomicAdd(&s_nl, 1)] = (uint32_t)kk;
+        }
+        __syncthreads();
+        // 4. exact small factors of both sides, then the stage-1 test
+        const int nl = s_nl;
+        const uint64_t sigma = e.m * e.r;
+        for (int li = tid; li < nl; li += blockDim.x) {
+            const uint32_t kk = s_list[li];
+            const uint64_t k = k0 + kk;
+            const uint64_t x = k * e.b;
+            const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
+            const bool vU = x >= a.n_first && x <= a.n_last;
+            bool pL = false, pU = false;
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+                const bool valid = side ? vL : vU;
+                if (!valid) continue;
+                const uint64_t y = side ? x - 1 : x + 1;
+                const int tz = __ffsll((long long)y) - 1;
+                uint64_t c = y >> tz, sy = tz ? 1ull << (tz - 1) : 1ull;
+                for (int w = 0; w < W; ++w) {
+                    uint32_t m = masks[(side * W + w) * kc + kk];
+                    while (m) {
+                        const int j = 32 * w + __ffs(m) - 1;
+                        m &= m - 1;
+                        const ulonglong2 d = s_il[j];
+                        c *= d.x;
+                        while (c * d.x <= d.y) { c *= d.x; sy *= s_p[j]; }
+                    }
+                }
+                const bool pass = twice_prod_ge(sigma, sy * surplus_bound(c, a), side ? x : x + 1);
+                if (side) pL = pass; else pU = pass;
+            }
+            if (pL || pU) {
+                const uint64_t radx = k * e.r;
+                const unsigned long long slot = atomicAdd(&a.ctr[CTR_SURV], (unsigned long long)(pL + pU));
+                if (pL && slot < a.q1_cap) a.q1[slot] = make_ulonglong2((x - 1) | (1ull << 63), radx);
+                const unsigned long long s2 = slot + pL;
+                if (pU && s2 < a.q1_cap) a.q1[s2] = make_ulonglong2(x, radx);
+            }
+        }
     }
 }
 
@@ -313,6 +482,12 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
 
 }  // namespace
 
+size_t heavy_sieve_smem(int np2, int kc, int ntasks) {
+    const int W = (np2 + 31) >> 5;
+    return sizeof(uint32_t) * (size_t)2 * W * kc + (sizeof(ulonglong2) + 2 * sizeof(uint32_t) + 2 * sizeof(int32_t)) * np2 +
+           sizeof(uint32_t) * ((size_t)ntasks + kc);
+}
+
 size_t heavy_scan_temp_bytes(uint64_t nent) {
     size_t bytes = 0;
     cub::DeviceScan::InclusiveSum(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)nent);
@@ -328,6 +503,15 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         cub::DeviceScan::InclusiveSum(scan_temp, bytes, a.cnt, a.incl, (int64_t)a.nent, st);
         const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint32_t));
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
+        if (a.kmin != ~0ull) {
+            const size_t smemS = heavy_sieve_smem(a.np2, a.kc, a.ntasks);
+            static size_t attr_set = 0;
+            if (smemS > 48 * 1024 && smemS > attr_set) {
+                cudaFuncSetAttribute(k_heavy_sieve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemS);
+                attr_set = smemS;
+            }
+            k_heavy_sieve<<<grid, 256, smemS, st>>>(a);
+        }
     }
     const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t));
     k_heavy_exact<<<grid, 256, smem3, st>>>(a);

@@ -60,12 +60,25 @@ struct TailArgs {
 constexpr int HEAVY_THREADS = 256;
 constexpr int HEAVY_NP2 = 512;   // odd primes <= y_max^(1/4) staged in shared memory
 constexpr int HEAVY_NP3 = 2048;  // odd primes <= cbrt(y_max) staged in shared memory
+// Classes with at least HEAVY_KMIN values of k in a domain are sieved over k (k_heavy_sieve)
+// in chunks of up to kc values; the rest go through trial division (k_heavy_screen).  Item
+// counts are packed: low 40 bits trial items, high 24 bits sieve chunks (one scan).
+constexpr uint64_t HEAVY_KMIN_DEFAULT = 512;
+constexpr uint64_t HEAVY_TRIAL_MASK = (1ull << 40) - 1;
+constexpr int HEAVY_TASK_HITS = 16;  // marks per sieve task (host-built task list)
 struct HeavyArgs {
     const BnxHeavyEnt* ent;
     uint64_t nent;
     uint64_t* cnt;    // per class: number of k in the domain
     uint64_t* incl;   // inclusive scan of cnt
     uint32_t* klo;    // per class: first k in the domain
+    uint32_t* kcnt;   // per class: number of k in the domain
+    const uint32_t* tasks;  // sieve marking tasks: j | side << 10 | r << 11 | R << 21
+    int ntasks;
+    int kc;                 // k values per sieve chunk
+    uint64_t kmin;          // classes with >= kmin k in the domain are sieved
+    const uint16_t* invtab; // per prime j <= P2: a^-1 mod p at invtab[invoff[j] + a]
+    const uint32_t* invoff;
     const uint32_t* kinfo;  // per k: bits 0..30 = primes 2..127 dividing k, bit 31 = k not squarefree
     uint64_t nkinfo;
     uint64_t x_lo, x_hi;    // heavy x range: [n_first, n_last + 1]
@@ -84,6 +97,7 @@ struct HeavyArgs {
     int* flags;             // [1] k outside kinfo (internal error)
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
+size_t heavy_sieve_smem(int np2, int kc, int ntasks);
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
                   cudaEvent_t ev_generated);
 

@@ -10,7 +10,8 @@ import argparse
 import csv
 import json
 
-GENERATOR = ("k_heavy_count", "DeviceScanInitKernel", "DeviceScanKernel", "k_heavy_screen", "k_heavy_exact")
+GENERATOR = ("k_heavy_count", "DeviceScanInitKernel", "DeviceScanKernel", "k_heavy_screen", "k_heavy_sieve",
+             "k_heavy_exact")
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "inst": 1, "": 1}
 
 
