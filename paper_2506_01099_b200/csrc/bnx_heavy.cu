@@ -127,7 +127,7 @@ struct HeavyItem {
 // The y tests of one heavy x (both sides), see the file comment.  Shared tables: (inv, lim)
 // and p of the odd primes <= P2.
 __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
-                                        const uint32_t* s_p) {
+                                        const uint32_t* s_p, const uint2* s_pd32) {
     const uint64_t x = it.x;
     const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
     const bool vU = x >= a.n_first && x <= a.n_last;
@@ -137,15 +137,28 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
     uint64_t sL = tL ? 1ull << (tL - 1) : 1ull, sU = tU ? 1ull << (tU - 1) : 1ull;
     // Divisibility of the odd parts by 32 primes at a time into bit masks (branch-free: the
     // lanes of a warp stay converged), then the hits (about 1.5 per y) are divided out fully.
+    // Both y below 2^32 (domains below 2^32): 32-bit tests, one IMAD per prime and side
+    // instead of a 64-bit multiply (the kernel is IMAD-pipe bound).
+    const bool narrow = yU < (1ull << 32);
     const uint64_t oL = cL, oU = cU;
+    const uint32_t oL32 = (uint32_t)oL, oU32 = (uint32_t)oU;
     for (int j0 = 0; j0 < a.np2; j0 += 32) {
         const int jn = min(32, a.np2 - j0);
         uint32_t mL = 0, mU = 0;
+        if (narrow) {
 #pragma unroll 8
-        for (int u = 0; u < jn; ++u) {
-            const ulonglong2 d = s_il[j0 + u];
-            mL |= (uint32_t)(oL * d.x <= d.y) << u;
-            mU |= (uint32_t)(oU * d.x <= d.y) << u;
+            for (int u = 0; u < jn; ++u) {
+                const uint2 d = s_pd32[j0 + u];
+                mL |= (uint32_t)(oL32 * d.x <= d.y) << u;
+                mU |= (uint32_t)(oU32 * d.x <= d.y) << u;
+            }
+        } else {
+#pragma unroll 8
+            for (int u = 0; u < jn; ++u) {
+                const ulonglong2 d = s_il[j0 + u];
+                mL |= (uint32_t)(oL * d.x <= d.y) << u;
+                mU |= (uint32_t)(oU * d.x <= d.y) << u;
+            }
         }
         while (mL | mU) {  // one hit of each side per round: the rounds are shared
             if (mL) {
@@ -182,14 +195,16 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
 // takes one and runs the y tests, so the expensive part always runs with full warps.
 __global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) {
     constexpr int T = HEAVY_THREADS;
-    extern __shared__ ulonglong2 s_il[];  // np2 (inv, lim), then np2 p
-    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + a.np2);
+    extern __shared__ ulonglong2 s_il[];  // np2 (inv, lim), np2 (inv32, lim32), np2 p
+    uint2* s_pd32 = reinterpret_cast<uint2*>(s_il + a.np2);
+    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + a.np2);
     __shared__ HeavyItem s_q[2 * T];
     __shared__ int s_cnt;
     __shared__ unsigned long long s_cls;
     const int tid = threadIdx.x;
     for (int j = tid; j < a.np2; j += T) {
         s_il[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
+        s_pd32[j] = make_uint2((uint32_t)a.pdiv[j].inv, 0xFFFFFFFFu / (uint32_t)a.pdiv[j].p);  // p^-1 mod 2^32
         s_p[j] = (uint32_t)a.pdiv[j].p;
     }
     if (tid == 0) s_cnt = 0;
@@ -231,7 +246,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) 
         }
         if (cnt == 0) break;
         const int take = min(cnt, T);
-        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p);
+        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p, s_pd32);
         cnt -= take;
         __syncthreads();
         if (tid == 0) s_cnt = cnt;
@@ -501,7 +516,7 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         k_heavy_count<<<cb, 256, 0, st>>>(a);
         size_t bytes = scan_temp_bytes;
         cub::DeviceScan::InclusiveSum(scan_temp, bytes, a.cnt, a.incl, (int64_t)a.nent, st);
-        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint32_t));
+        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (a.kmin != ~0ull) {
             const size_t smemS = heavy_sieve_smem(a.np2, a.kc, a.ntasks);
