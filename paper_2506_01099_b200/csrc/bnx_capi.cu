@@ -137,6 +137,8 @@ struct bnx_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    cudaStream_t aux = nullptr;  // second stream: k_tail_heavy beside k_tail (heavy engine)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     int num_sms = 148;
     int screen_blocks_per_sm = 1;
     int screen_v = 0;
@@ -560,13 +562,22 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.q1_cap = c->q1.cap;
     ha.cand = c->cand.p;
     ha.cand_cap = c->cand.cap;
+    ha.heavy = c->heavy.p;
+    ha.heavy_cap = c->heavy.cap;
+    ha.kinds = kinds;
     ha.ctr = c->ctr.p;
     ha.flags = c->flags.p;
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * 8, c->stream, c->timing ? c->ev[1] : nullptr);
     TailArgs ta{nullptr, 0, c->cand.p, c->cand.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p,
                 c->pairs.cap, c->ctr.p};
-    launch_tail(ta, grid_for(c), c->stream);
+    // k_tail_heavy (the few candidates with many residue-class members) overlaps k_tail
+    CK(cudaEventRecord(c->fork_ev, c->stream));
+    CK(cudaStreamWaitEvent(c->aux, c->fork_ev, 0));
+    launch_tail_heavy(ta, c->aux);
+    CK(cudaEventRecord(c->join_ev, c->aux));
+    launch_tail_light(ta, grid_for(c), c->stream);
+    CK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
     CK(cudaGetLastError());
     if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
     CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
@@ -637,7 +648,7 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
         if (c->h_flags[1]) return fail(BNX_ERR_CUDA, "heavy generator: k outside its table");
         if (c->engine == 0) {
             if (h[CTR_SURV] > c->q1.cap) { TRY(c->q1.ensure(h[CTR_SURV] * 2)); again = true; }
-            if (h[CTR_CAND] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_CAND] * 2)); again = true; }
+            if (h[CTR_LIGHT] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_LIGHT] * 2)); again = true; }
         } else if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
         if (h[CTR_HEAVY] > c->heavy.cap) { TRY(c->heavy.ensure(h[CTR_HEAVY] * 2)); again = true; }
         if (h[CTR_PAIRS] > c->pairs.cap) { TRY(c->pairs.ensure(h[CTR_PAIRS] * 2)); again = true; }
@@ -711,6 +722,9 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
+    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
@@ -760,6 +774,9 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    if (c->join_ev) cudaEventDestroy(c->join_ev);
     delete c;
     return BNX_OK;
 }

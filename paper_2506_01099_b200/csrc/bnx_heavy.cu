@@ -422,6 +422,26 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
     }
 }
 
+// A candidate goes to k_tail's list, or (more than TAIL_HEAVY residue-class members) to the
+// queue of k_tail_heavy, which runs concurrently on a second stream; the residue-class
+// counters are kept here (the member count as in k_tail).
+__device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand c) {
+    const uint64_t R = c.r0 * c.r1;
+    const uint64_t t1 = (a.kinds & 1u) ? (c.n - 1) / R : 0;
+    const uint64_t t0 = (c.n + 1) / R + 1, t2 = (2 * c.n) / R;
+    const uint64_t total = t1 + (((a.kinds & 2u) && t2 >= t0) ? t2 - t0 + 1 : 0);
+    atomicAdd(&a.ctr[CTR_CAND], 1ull);
+    if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
+    atomicMax(&a.ctr[CTR_MAXCHK], (unsigned long long)total);
+    if (total > TAIL_HEAVY) {
+        const unsigned long long h = atomicAdd(&a.ctr[CTR_HEAVY], 1ull);
+        if (h < a.heavy_cap) a.heavy[h] = c;
+    } else {
+        const unsigned long long slot = atomicAdd(&a.ctr[CTR_LIGHT], 1ull);
+        if (slot < a.cand_cap) a.cand[slot] = c;
+    }
+}
+
 // Exact radical of the other side (one thread per survivor: the odd primes <= cbrt(y_max)
 // from shared memory, 32 per bit mask as in y_tests; the cofactor is then 1, p, p^2 or pq),
 // the exact test R <= 2n, de-duplication, emission.
@@ -451,8 +471,7 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
                 const uint64_t sy = y / rady;
                 if (__umul64hi(2 * sy, sy) != 0 || 2 * sy * sy >= y) continue;
             }
-            const unsigned long long slot = atomicAdd(&a.ctr[CTR_CAND], 1ull);
-            if (slot < a.cand_cap) a.cand[slot] = sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady};
+            emit_candidate(a, sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady});
         }
         return;
     }
@@ -490,8 +509,7 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
             const uint64_t sy = y / rady;
             if (__umul64hi(2 * sy, sy) != 0 || 2 * sy * sy >= y) continue;
         }
-        const unsigned long long slot = atomicAdd(&a.ctr[CTR_CAND], 1ull);
-        if (slot < a.cand_cap) a.cand[slot] = sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady};
+        emit_candidate(a, sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady});
     }
 }
 

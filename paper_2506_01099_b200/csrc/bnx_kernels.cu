@@ -434,13 +434,10 @@ __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_be
     }
 }
 
-// Candidates with more than this many residue-class members are handed to k_tail_heavy,
-// which spreads their members over many warps (one candidate below 2^32 has ~1,500).
-constexpr uint64_t TAIL_HEAVY = 128;
 
 __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
     const int lane = threadIdx.x & 31;
-    const uint64_t cnt = a.cands ? min((uint64_t)a.ctr[CTR_CAND], a.cand_cap)
+    const uint64_t cnt = a.cands ? min((uint64_t)a.ctr[CTR_LIGHT], a.cand_cap)
                                  : min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
     for (;;) {
         // survivors / candidates are taken one at a time from a shared counter
@@ -465,12 +462,12 @@ __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
         const uint64_t t2 = (2 * n) / c.R;
         const uint64_t c2 = ((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0;
         const uint64_t total = c.t1 + c2;
-        if (lane == 0) {
-            if (!a.cands) atomicAdd(&a.ctr[CTR_CAND], 1ull);
+        if (lane == 0 && !a.cands) {  // (heavy engine: counted and routed by k_heavy_exact)
+            atomicAdd(&a.ctr[CTR_CAND], 1ull);
             if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
             atomicMax(&a.ctr[CTR_MAXCHK], (unsigned long long)total);
         }
-        if (total > TAIL_HEAVY) {
+        if (total > TAIL_HEAVY && !a.cands) {
             bool queued = false;
             if (lane == 0) {
                 const unsigned long long h = atomicAdd(&a.ctr[CTR_HEAVY], 1ull);
@@ -800,6 +797,10 @@ void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st) {
 }
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
     k_tail<<<grid, 256, 0, st>>>(a);
+    k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);
+}
+void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st) { k_tail<<<grid, 256, 0, st>>>(a); }
+void launch_tail_heavy(const TailArgs& a, cudaStream_t st) {
     k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);
 }
 

@@ -21,8 +21,12 @@ constexpr int SIEVE_MAXS = 160;
 // Counter block (device): [0] survivors [1] candidates [2] residue checks [3] matches [4] pairs
 // [5] the tail's work queue head [6] most residue-class members of one candidate
 // [7] heavy candidates queued for k_tail_heavy
+// [8] heavy engine: candidates in the light list (k_tail); the rest went to the heavy queue
 constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_NEXT = 5, CTR_MAXCHK = 6,
-              CTR_HEAVY = 7, CTR_N = 8;
+              CTR_HEAVY = 7, CTR_LIGHT = 8, CTR_N = 9;
+// Candidates with more than this many residue-class members are handed to k_tail_heavy,
+// which spreads their members over many warps (one candidate below 2^32 has ~1,500).
+constexpr uint64_t TAIL_HEAVY = 128;
 
 struct ScreenArgs {
     uint64_t x_begin;  // multiple of the tile
@@ -91,8 +95,11 @@ struct HeavyArgs {
     int cube_filter;        // P2 >= 7: cube residues mod 63 pre-filter the p^3 test
     ulonglong2* q1;         // screen survivors: (n | side << 63, rad x)
     uint64_t q1_cap;
-    BnxCand* cand;          // exact candidates
+    BnxCand* cand;          // exact candidates with <= TAIL_HEAVY residue-class members (k_tail)
     uint64_t cand_cap;
+    BnxCand* heavy;         // the others (k_tail_heavy, concurrently on a second stream)
+    uint64_t heavy_cap;
+    uint32_t kinds;
     unsigned long long* ctr;
     int* flags;             // [1] k outside kinfo (internal error)
 };
@@ -149,6 +156,8 @@ size_t sieve_smem_bytes();
 const void* sieve_kernel();
 void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st);
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st);
+void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st);  // heavy engine: k_tail only
+void launch_tail_heavy(const TailArgs& a, cudaStream_t st);            // heavy engine: k_tail_heavy only
 void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st);
 void launch_prime_seg(uint64_t lo, uint64_t hi, const uint32_t* base, uint32_t nbase, uint32_t* counts,
                       const uint64_t* offsets, uint32_t* out, uint64_t nblocks, cudaStream_t st);
