@@ -446,11 +446,13 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
 // from shared memory, 32 per bit mask as in y_tests; the cofactor is then 1, p, p^2 or pq),
 // the exact test R <= 2n, de-duplication, emission.
 __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
-    extern __shared__ ulonglong2 s_il3[];  // np3 (inv, lim), then np3 p
-    uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_il3 + a.np3);
+    extern __shared__ ulonglong2 s_il3[];  // np3 (inv, lim), np3 (inv32, lim32), np3 p
+    uint2* s_pd3 = reinterpret_cast<uint2*>(s_il3 + a.np3);
+    uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_pd3 + a.np3);
     const int np3 = (int)a.np3;
     for (int j = threadIdx.x; j < np3; j += blockDim.x) {
         s_il3[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
+        s_pd3[j] = make_uint2((uint32_t)a.pdiv[j].inv, 0xFFFFFFFFu / (uint32_t)a.pdiv[j].p);
         s_p3[j] = (uint32_t)a.pdiv[j].p;
     }
     __syncthreads();
@@ -483,13 +485,22 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         const int tz = __ffsll((long long)y) - 1;
         const uint64_t o = y >> tz;
         uint64_t c = o, rady = tz ? 2 : 1;
+        const bool narrow = o < (1ull << 32);  // 32-bit tests (see y_tests)
         for (int j0 = 0; j0 < np3; j0 += 32) {
             const int jn = min(32, np3 - j0);
             uint32_t m = 0;
+            if (narrow) {
 #pragma unroll 8
-            for (int u = 0; u < jn; ++u) {
-                const ulonglong2 d = s_il3[j0 + u];
-                m |= (uint32_t)(o * d.x <= d.y) << u;
+                for (int u = 0; u < jn; ++u) {
+                    const uint2 d = s_pd3[j0 + u];
+                    m |= (uint32_t)((uint32_t)o * d.x <= d.y) << u;
+                }
+            } else {
+#pragma unroll 8
+                for (int u = 0; u < jn; ++u) {
+                    const ulonglong2 d = s_il3[j0 + u];
+                    m |= (uint32_t)(o * d.x <= d.y) << u;
+                }
             }
             while (m) {
                 const int u = __ffs(m) - 1;
@@ -546,7 +557,12 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
             k_heavy_sieve<<<grid, 256, smemS, st>>>(a);
         }
     }
-    const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t));
+    const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
+    static size_t attr3 = 0;
+    if (smem3 > 48 * 1024 && smem3 > attr3) {
+        cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+        attr3 = smem3;
+    }
     k_heavy_exact<<<grid, 256, smem3, st>>>(a);
     if (ev_generated) cudaEventRecord(ev_generated, st);
 }
