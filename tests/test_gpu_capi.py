@@ -93,3 +93,20 @@ def test_domain_search_equals_filtered_full(L, ctx):
     assert L.bnx_search(ctx, 5_000_001, 3, None, 0, 0, buf, 64, ctypes.byref(found)) == 0
     full = sorted(((r.m, r.n) for r in buf[: found.value] if r.n >= 1000), key=lambda x: (x[1], x[0]))
     assert dom == full
+
+
+def test_engine_selection(L, ctx):
+    """bnx_ctx_set_engine / bnx_ctx_engine: both generators through the C ABI, same rows;
+    unknown engines are rejected with BNX_ERR_INVALID and leave the engine unchanged."""
+    assert L.bnx_ctx_engine(ctx) == 0  # heavy by default
+    found = ctypes.c_size_t(0)
+    rows = {}
+    for eng in (1, 0):
+        assert L.bnx_ctx_set_engine(ctx, eng) == 0
+        assert L.bnx_ctx_engine(ctx) == eng
+        buf = (_native.PairRow * 64)()
+        assert L.bnx_search(ctx, 1 << 24, 3, None, 0, 0, buf, 64, ctypes.byref(found)) == 0
+        rows[eng] = [(r.m, r.n, r.rad_m, r.rad_m1, r.kind) for r in buf[: found.value]]
+    assert rows[0] == rows[1] and len(rows[0]) == 25
+    assert L.bnx_ctx_set_engine(ctx, 7) == 4
+    assert L.bnx_ctx_engine(ctx) == 0
