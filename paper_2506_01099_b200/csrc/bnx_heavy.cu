@@ -141,17 +141,20 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
     // instead of a 64-bit multiply (the kernel is IMAD-pipe bound).
     const bool narrow = yU < (1ull << 32);
     const uint64_t oL = cL, oU = cU;
-    const uint32_t oL32 = (uint32_t)oL, oU32 = (uint32_t)oU;
+    const uint32_t x32 = (uint32_t)x;
     for (int j0 = 0; j0 < a.np2; j0 += 32) {
         const int jn = min(32, a.np2 - j0);
         uint32_t mL = 0, mU = 0;
         if (narrow) {
+            // one multiply per prime for both sides: (x -+ 1) p^-1 = x p^-1 -+ p^-1 (mod 2^32)
 #pragma unroll 8
             for (int u = 0; u < jn; ++u) {
                 const uint2 d = s_pd32[j0 + u];
-                mL |= (uint32_t)(oL32 * d.x <= d.y) << u;
-                mU |= (uint32_t)(oU32 * d.x <= d.y) << u;
+                const uint32_t t = x32 * d.x;
+                mL |= (uint32_t)(t - d.x <= d.y) << u;
+                mU |= (uint32_t)(t + d.x <= d.y) << u;
             }
+            mL = vL ? mL : 0u;
         } else {
 #pragma unroll 8
             for (int u = 0; u < jn; ++u) {
