@@ -1,0 +1,55 @@
+"""Both kinds below S on one B200 with the heavy generator, for S beyond the paper's range
+(1.4e12): every pair found is re-verified on the CPU (exact radicals of m, m+1, n, n+1 by
+trial division) and compared with the known infinite families (families.py); one JSON line
+per bound.
+
+    python scripts/beyond_paper.py 2^42 2^43 2^44
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2506_01099_b200 as bp  # noqa: E402
+from paper_2506_01099_b200 import _native  # noqa: E402
+
+
+def parse(v: str) -> int:
+    return 2 ** int(v[2:]) if v.startswith("2^") else int(float(v))
+
+
+ctx = _native.context(0)
+ctx.set_timing(True)
+for arg in sys.argv[1:] or ["2^44"]:
+    S = parse(arg)
+    t0 = time.perf_counter()
+    ctx.prepare(S)
+    t_prep = time.perf_counter() - t0
+    ctx.enqueue(1, S - 1, 3)
+    rows = ctx.collect()
+    gen_ms, pipe_ms = ctx.timing()
+    st = ctx.stats()
+    ctx.enqueue(1, S - 1, 3)  # second run: timing with warm tables
+    rows2 = ctx.collect()
+    gen2, pipe2 = ctx.timing()
+    pairs = sorted((int(r["m"]), int(r["n"]), int(r["kind"])) for r in rows)
+    verified = all(
+        (bp.radical_oracle(m), bp.radical_oracle(m + 1)) ==
+        ((bp.radical_oracle(n), bp.radical_oracle(n + 1)) if k == 1 else (bp.radical_oracle(n + 1), bp.radical_oracle(n)))
+        for m, n, k in pairs)
+    # the known families (families.py) continued past the completeness bound
+    from paper_2506_01099_b200 import families as fm
+    known = [(m, n, 1) for m, n in (fm.family_first_kind(k) for k in range(2, 32)) if n < S]
+    known += [(m, n, 2) for m, n in (fm.family_second_kind(k) for k in range(0, 32)) if n < S]
+    known += [(p.m, p.n, int(p.kind)) for p in fm.exceptional_pairs() if p.n < S]
+    known.sort()
+    extra = [p for p in pairs if p not in known]
+    missing = [p for p in known if p not in pairs]
+    print(json.dumps({"S": S, "pairs": len(pairs), "first": sum(k == 1 for *_, k in pairs),
+                      "second": sum(k == 2 for *_, k in pairs), "verified_on_cpu": verified,
+                      "families_known": len(known), "missing_family_members": missing,
+                      "pairs_outside_the_families": extra, "same_on_rerun": len(rows2) == len(rows),
+                      "device_ms": pipe2, "generator_ms": gen2, "first_run_device_ms": pipe_ms,
+                      "table_build_s": t_prep, "survivors": st["survivors"],
+                      "candidates": st["candidates"]}), flush=True)

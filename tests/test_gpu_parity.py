@@ -234,6 +234,17 @@ def test_heavy_candidates_on_random_domains(orc):
         assert bp.last_stats()["candidates"] == exact_candidates(orc, lo, hi), (lo, hi)
 
 
+def test_heavy_candidates_beyond_the_paper(orc):
+    """Windows between 2^42 and 2^44 (beyond the byte screen's range and the paper's 1.4e12):
+    the heavy generator's exact candidate count equals the oracle's sieve count."""
+    rng = np.random.default_rng(9)
+    for _ in range(4):
+        lo = int(rng.integers(2**42, 2**44 - 2**22))
+        hi = lo + (1 << 21)
+        bp.search_domain(lo, hi)
+        assert bp.last_stats()["candidates"] == exact_candidates(orc, lo, hi), (lo, hi)
+
+
 @pytest.mark.parametrize("lo,hi", [(1, 2**32 - 1), (2**32, 2**33 - 1), (2**40 - 2**30, 2**40 - 1),
                                    (1_400_000_000_000 - 2**28, 1_400_000_000_000), (2**42 - 2**26, 2**42 - 2)])
 def test_engines_agree(lo, hi):
@@ -266,15 +277,18 @@ def test_random_domains_vs_oracle(orc):
 
 
 def test_near_the_top_of_the_range():
-    """Largest supported bounds (< 2^42): the first-kind family member k = 21,
-    (2^21 - 2, 2^42 - 2^22), lies just below 2^42 and must be found with its radicals."""
-    m, n = 2**21 - 2, 2**42 - 2**22
-    got = bp.search_domain(n - 5000, n + 5000)
-    assert [(int(p.kind), p.m, p.n) for p in got] == [(1, m, n)]
-    p = got[0]
-    assert (p.rad_m, p.rad_m_plus_1) == (bp.radical_oracle(m), bp.radical_oracle(m + 1))
-    with pytest.raises(ValueError):
-        bp.search_domain(2**42 - 10, 2**42)
+    """Largest supported bounds: the first-kind family member (2^k - 2, 2^(2k) - 2^(k+1)) just
+    below the top must be found with its radicals -- k = 22 below 2^44 with the heavy
+    generator, k = 21 below 2^42 with the byte screen -- and larger bounds are refused."""
+    for name, k, top in (("heavy", 22, 2**44), ("screen", 21, 2**42)):
+        with engine(name):
+            m, n = 2**k - 2, 2**(2 * k) - 2**(k + 1)
+            got = bp.search_domain(n - 5000, n + 5000)
+            assert [(int(p.kind), p.m, p.n) for p in got] == [(1, m, n)], name
+            p = got[0]
+            assert (p.rad_m, p.rad_m_plus_1) == (bp.radical_oracle(m), bp.radical_oracle(m + 1))
+            with pytest.raises(ValueError):
+                bp.search_domain(top - 10, top + 1)
 
 
 def test_repeated_searches_are_identical():
