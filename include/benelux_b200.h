@@ -111,6 +111,12 @@ BNX_API int bnx_ctx_set_timing(bnx_ctx_t* ctx, int enabled);
 #define BNX_ENGINE_SCREEN 1
 BNX_API int bnx_ctx_set_engine(bnx_ctx_t* ctx, int engine);
 BNX_API int bnx_ctx_engine(const bnx_ctx_t* ctx);
+/* Multi-GPU: subsequent searches on this context compute only shard `shard` of `nshards`
+ * (0 <= shard < nshards); the row sets of the shards of one search are disjoint and their
+ * union is the full result.  The heavy generator splits its (surplus class, k) items and
+ * sieve chunks evenly (balanced work: heavy integers thin out as n grows); the byte screen
+ * splits the n-range into contiguous slabs.  Default 0 of 1. */
+BNX_API int bnx_ctx_set_shard(bnx_ctx_t* ctx, uint32_t shard, uint32_t nshards);
 BNX_API int bnx_ctx_timing(const bnx_ctx_t* ctx, float* screen_ms, float* pipeline_ms);
 
 /* primes.py:24-35: all primes <= limit, ascending.  *count always receives the total;

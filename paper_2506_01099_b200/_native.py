@@ -29,7 +29,7 @@ ENGINES = {"heavy": 0, "screen": 1}  # bnx_ctx_set_engine (include/benelux_b200.
 # Every symbol include/benelux_b200.h declares (tests check the library exports them all).
 EXPORTED_SYMBOLS = (
     "bnx_version", "bnx_last_error", "bnx_device_count", "bnx_ctx_create", "bnx_ctx_destroy",
-    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_primes_up_to", "bnx_sieve_radicals",
+    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_ctx_set_shard", "bnx_primes_up_to", "bnx_sieve_radicals",
     "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain",
     "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of", "bnx_brute_force",
     "bnx_table_create", "bnx_table_destroy", "bnx_table_insert_all", "bnx_table_probe_all", "bnx_table_slots",
@@ -112,6 +112,7 @@ def load() -> ctypes.CDLL:
         L.bnx_ctx_set_timing.argtypes = [vp, ctypes.c_int]
         L.bnx_ctx_set_engine.argtypes = [vp, ctypes.c_int]
         L.bnx_ctx_engine.argtypes = [vp]
+        L.bnx_ctx_set_shard.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32]
         L.bnx_ctx_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
         L.bnx_primes_up_to.argtypes = [vp, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_sieve_radicals.argtypes = [
@@ -204,6 +205,11 @@ class Context:
         code = ENGINES[engine] if isinstance(engine, str) else int(engine)
         with self.lock:
             check(load().bnx_ctx_set_engine(self.handle, code))
+
+    def set_shard(self, shard: int, nshards: int) -> None:
+        """Multi-GPU: later searches compute shard `shard` of `nshards` (include/benelux_b200.h)."""
+        with self.lock:
+            check(load().bnx_ctx_set_shard(self.handle, shard, nshards))
 
     def engine(self) -> str:
         code = load().bnx_ctx_engine(self.handle)

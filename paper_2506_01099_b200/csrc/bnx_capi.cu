@@ -156,6 +156,7 @@ struct bnx_ctx {
     HeavyTab heavy_tab;
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
     uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
+    uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
     DBuf<ulonglong2> q1;
     DBuf<BnxCand> cand;
 
@@ -567,6 +568,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.kinds = kinds;
     ha.ctr = c->ctr.p;
     ha.flags = c->flags.p;
+    ha.shard = c->shard;
+    ha.nshards = c->nshards;
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * 8, c->stream, c->timing ? c->ev[1] : nullptr);
     TailArgs ta{nullptr, 0, c->cand.p, c->cand.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p,
@@ -593,8 +596,24 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     return BNX_OK;
 }
 
+int empty_search(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds);
+int enqueue_screen(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds);
+
 int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     if (c->engine == 0) return enqueue_heavy(c, n_first, n_last, kinds);
+    if (c->nshards == 1) return enqueue_screen(c, n_first, n_last, kinds);
+    // byte screen: the shard is a contiguous slab of n (the recorded domain stays the full
+    // one, so a capacity retry re-shards it identically)
+    const uint64_t total = n_last - n_first + 1;
+    const uint64_t lo = n_first + total * c->shard / c->nshards;
+    const uint64_t hi = n_first + total * (c->shard + 1) / c->nshards;  // exclusive
+    TRY(lo < hi ? enqueue_screen(c, lo, hi - 1, kinds) : empty_search(c, n_first, n_last, kinds));
+    c->q_first = n_first;
+    c->q_last = n_last;
+    return BNX_OK;
+}
+
+int enqueue_screen(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     Tables& t = c->screen_tab;
     TRY(ensure_work(c));
     const ScreenVariant& sv = screen_variant(c->screen_v);
@@ -622,6 +641,26 @@ int enqueue(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     c->stats = bnx_stats_t{};
     c->stats.integers = n_last - n_first + 1;
     c->stats.kernel_launches = 3;
+    return BNX_OK;
+}
+
+// A search with nothing to do (an empty shard): zeroed counters, no launches.
+int empty_search(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
+    TRY(ensure_work(c));
+    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+    CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+    CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (c->timing) {
+        CK(cudaEventRecord(c->ev[0], c->stream));
+        CK(cudaEventRecord(c->ev[1], c->stream));
+        CK(cudaEventRecord(c->ev[2], c->stream));
+    }
+    c->q_valid = true;
+    c->q_first = n_first;
+    c->q_last = n_last;
+    c->q_kinds = kinds;
+    c->stats = bnx_stats_t{};
     return BNX_OK;
 }
 
@@ -827,6 +866,15 @@ int bnx_ctx_set_engine(bnx_ctx_t* c, int engine) {
 }
 
 int bnx_ctx_engine(const bnx_ctx_t* c) { return c ? c->engine : -1; }
+
+int bnx_ctx_set_shard(bnx_ctx_t* c, uint32_t shard, uint32_t nshards) {
+    if (!c) return fail(BNX_ERR_INVALID, "null context");
+    if (nshards < 1 || shard >= nshards || nshards > (1u << 20)) return fail(BNX_ERR_INVALID, "bad shard");
+    if (c->q_valid) return fail(BNX_ERR_INVALID, "a search is enqueued");
+    c->shard = shard;
+    c->nshards = nshards;
+    return BNX_OK;
+}
 
 int bnx_ctx_timing(const bnx_ctx_t* c, float* screen_ms, float* pipeline_ms) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");

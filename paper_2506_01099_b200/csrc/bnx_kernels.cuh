@@ -102,6 +102,7 @@ struct HeavyArgs {
     uint32_t kinds;
     unsigned long long* ctr;
     int* flags;             // [1] k outside kinfo (internal error)
+    uint32_t shard, nshards;  // this search covers items/chunks [shard, shard + 1) / nshards
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
 size_t heavy_sieve_smem(int np2, int kc, int ntasks);

@@ -1,11 +1,14 @@
-"""Multi-GPU search: one process per GPU, the n-range sharded into contiguous slabs.
+"""Multi-GPU search: one process per GPU, no data-path exchange.
 
-The search shards with no data-path exchange: a pair (m, n) is found by the rank that owns
-n, because every partner m of n is reached through the residue classes of
-R = rad(n) rad(n+1) and verified exactly on that rank (no other rank's data is needed;
-see DESIGN.md section "Multi-GPU").  The only collective is the final gather of the verified
-rows (a few dozen 40-byte records) so every rank returns the same sorted list, which is
-independent of the number of ranks.
+A pair (m, n) is found from its candidate n alone: every partner m of n is reached through
+the residue classes of R = rad(n) rad(n+1) and verified exactly on the same rank (no other
+rank's data is needed; see DESIGN.md section "Multi-GPU").  So the work splits two ways:
+  * "items" (default with the device search): every rank runs the whole domain but its
+    generator walks only 1/world of the (surplus class, k) items and sieve chunks
+    (bnx_ctx_set_shard) -- balanced, since heavy integers thin out as n grows;
+  * "slabs": contiguous slabs of n (shard_domain), as the reference's chunking would split.
+The only collective is the final gather of the verified rows (a few dozen 40-byte records)
+so every rank returns the same sorted list, which is independent of the number of ranks.
 
 torch.distributed is the plumbing (NCCL on GPUs, gloo in the CPU tests).
 """
@@ -65,19 +68,34 @@ def gather_rows(local: np.ndarray, group=None) -> np.ndarray:
 
 
 def find_pairs_distributed(limit: int, *, kinds=None, device: int | None = None, group=None,
-                           searcher: Searcher | None = None) -> list[BeneluxPair]:
+                           searcher: Searcher | None = None, balance: str | None = None) -> list[BeneluxPair]:
     """Every pair m < n < limit, computed by all ranks of `group`; every rank returns the
-    same list sorted by (m, n).  `searcher` overrides the device search (tests)."""
+    same list sorted by (m, n).  `balance` is "items" (default for the device search) or
+    "slabs"; `searcher` overrides the device search (tests, slabs only)."""
     import torch.distributed as dist
 
     if limit < 3:
         raise ValueError("limit must be >= 3")
+    balance = balance or ("slabs" if searcher else "items")
+    if balance not in ("items", "slabs") or (balance == "items" and searcher):
+        raise ValueError(f"bad balance {balance!r}")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    run = searcher or _device_searcher(kinds, device)
     from ._native import PAIR_DTYPE
 
-    dom = shard_domain(1, limit - 1, rank, world)
-    local = run(*dom) if dom else np.empty(0, PAIR_DTYPE)
+    if balance == "items":
+        from . import _native
+        from .search import search_rows
+
+        ctx = _native.context(device)
+        ctx.set_shard(rank, world)
+        try:
+            local = search_rows(1, limit - 1, kinds=kinds, device=device)
+        finally:
+            ctx.set_shard(0, 1)
+    else:
+        run = searcher or _device_searcher(kinds, device)
+        dom = shard_domain(1, limit - 1, rank, world)
+        local = run(*dom) if dom else np.empty(0, PAIR_DTYPE)
     rows = gather_rows(np.ascontiguousarray(local, dtype=PAIR_DTYPE), group)
     order = np.lexsort((rows["n"], rows["m"]))
     return pairs_from_rows(rows[order])

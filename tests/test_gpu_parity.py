@@ -291,6 +291,27 @@ def test_near_the_top_of_the_range():
                 bp.search_domain(top - 10, top + 1)
 
 
+@pytest.mark.parametrize("name", ["heavy", "screen"])
+def test_shards_partition_the_search(name):
+    """bnx_ctx_set_shard: the shards of one search return disjoint row sets whose union is
+    the full search (heavy: item shards; screen: n-slabs), for several shard counts."""
+    ctx = bp._native.context(None)
+    lo, hi = 1, 2**32 - 1
+    with engine(name):
+        full = sorted(map(tuple, bp.search.search_rows(lo, hi).tolist()))
+        try:
+            for nsh in (2, 3, 7):
+                parts = []
+                for sh in range(nsh):
+                    ctx.set_shard(sh, nsh)
+                    parts += list(map(tuple, bp.search.search_rows(lo, hi).tolist()))
+                assert sorted(parts) == full, nsh
+        finally:
+            ctx.set_shard(0, 1)
+    with pytest.raises(ValueError):
+        ctx.set_shard(3, 3)
+
+
 def test_repeated_searches_are_identical():
     """Back-to-back device searches (the bench's pattern) give identical rows and counters:
     guards the CTA-level work queue of k_heavy_screen against barrier/race bugs."""
