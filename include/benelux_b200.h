@@ -146,6 +146,14 @@ BNX_API int bnx_search(bnx_ctx_t* ctx, uint64_t limit, uint32_t kinds_mask, cons
 
 /* chunked.py:307-359: every pair (m, n), m < n, with n_first <= n <= n_last (any m >= 1).
  * Rows sorted by (n, m) (chunked.py:358). */
+/* The survey's multi-GPU entry point (one host thread drives ndev GPUs):
+ * context i on devices[i] (a process-wide pool) computes shard i of ndev of the search below
+ * `limit` (bnx_ctx_set_shard), all shards run concurrently, and the rows are merged and
+ * sorted by (m, n) -- identical to bnx_search for any device list.  A device may appear
+ * more than once (several shards on one GPU). */
+BNX_API int bnx_search_multi(const int* devices, int ndev, uint64_t limit, uint32_t kinds_mask,
+                             const uint64_t* primes, size_t nprimes, uint64_t primes_limit, bnx_pair_t* out,
+                             size_t cap, size_t* found);
 BNX_API int bnx_search_domain(bnx_ctx_t* ctx, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask,
                       const uint64_t* primes, size_t nprimes, uint64_t primes_limit, bnx_pair_t* out,
                       size_t cap, size_t* found);

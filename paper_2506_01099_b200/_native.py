@@ -30,7 +30,7 @@ ENGINES = {"heavy": 0, "screen": 1}  # bnx_ctx_set_engine (include/benelux_b200.
 EXPORTED_SYMBOLS = (
     "bnx_version", "bnx_last_error", "bnx_device_count", "bnx_ctx_create", "bnx_ctx_destroy",
     "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_ctx_set_shard", "bnx_primes_up_to", "bnx_sieve_radicals",
-    "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain",
+    "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain", "bnx_search_multi",
     "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of", "bnx_brute_force",
     "bnx_table_create", "bnx_table_destroy", "bnx_table_insert_all", "bnx_table_probe_all", "bnx_table_slots",
     "bnx_table_search_chunk",
@@ -126,6 +126,7 @@ def load() -> ctypes.CDLL:
         ]
         L.bnx_search.argtypes = search_args
         L.bnx_search_domain.argtypes = [vp, ctypes.c_uint64] + search_args[1:]
+        L.bnx_search_multi.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int] + search_args[1:]
         L.bnx_brute_force.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(PairRow), ctypes.c_size_t,
                                       ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_table_create.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
@@ -319,3 +320,25 @@ def context(device: int | None = None) -> Context:
             ctx = Context(device)
             _contexts[device] = ctx
         return ctx
+
+
+def search_multi(devices, limit: int, kinds: int, primes: np.ndarray | None = None, primes_limit: int = 0) -> np.ndarray:
+    """bnx_search_multi: one host thread drives every device in `devices` (a shard each);
+    rows sorted by (m, n), identical to a single-device search."""
+    L = load()
+    devs = (ctypes.c_int * len(devices))(*devices)
+    keep, pp, np_ = _prime_args(primes)  # noqa: F841 (keeps the array alive)
+    cap = 256
+    while True:
+        buf = (PairRow * cap)()
+        found = ctypes.c_size_t(0)
+        with _MULTI_LOCK:
+            st = check(L.bnx_search_multi(devs, len(devices), limit, kinds, pp, np_, primes_limit, buf, cap,
+                                          ctypes.byref(found)))
+        if st == BNX_BUFFER_FULL:
+            cap = int(found.value)
+            continue
+        return np.frombuffer(buf, dtype=PAIR_DTYPE, count=int(found.value)).copy()
+
+
+_MULTI_LOCK = threading.Lock()

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1031,6 +1032,47 @@ int bnx_search(bnx_ctx_t* c, uint64_t limit, uint32_t kinds_mask, const uint64_t
     if (limit < 3) return fail(BNX_ERR_INVALID, "limit must be >= 3");
     std::vector<bnx_pair_t> rows;
     TRY(search_rows(c, 1, limit - 1, kinds_mask, primes, nprimes, primes_limit, rows));
+    std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
+        return a.m != b.m ? a.m < b.m : a.n < b.n;
+    });
+    return emit(rows, out, cap, found);
+}
+
+// One host thread drives several GPUs: context i (device devices[i], a process-wide pool) runs
+// shard i of ndev of the search; all shards are enqueued before any is collected.
+static std::mutex g_multi_mu;
+static std::vector<bnx_ctx*> g_multi;
+
+int bnx_search_multi(const int* devices, int ndev, uint64_t limit, uint32_t kinds_mask, const uint64_t* primes,
+                     size_t nprimes, uint64_t primes_limit, bnx_pair_t* out, size_t cap, size_t* found) {
+    if (!devices || ndev < 1 || ndev > 1024) return fail(BNX_ERR_INVALID, "bad device list");
+    if (limit < 3) return fail(BNX_ERR_INVALID, "limit must be >= 3");
+    if ((kinds_mask & 3u) == 0) return fail(BNX_ERR_INVALID, "kinds_mask selects no kind");
+    std::lock_guard<std::mutex> lock(g_multi_mu);
+    if (g_multi.size() < (size_t)ndev) g_multi.resize(ndev, nullptr);
+    for (int i = 0; i < ndev; ++i) {
+        if (g_multi[i] && g_multi[i]->device != devices[i]) {
+            bnx_ctx_destroy(g_multi[i]);
+            g_multi[i] = nullptr;
+        }
+        if (!g_multi[i]) TRY(bnx_ctx_create(devices[i], &g_multi[i]));
+        bnx_ctx* c = g_multi[i];
+        TRY(activate(c));
+        c->shard = (uint32_t)i;
+        c->nshards = (uint32_t)ndev;
+        TRY(prepare(c, limit, primes, nprimes, primes_limit));
+    }
+    for (int i = 0; i < ndev; ++i) {
+        TRY(activate(g_multi[i]));
+        TRY(enqueue(g_multi[i], 1, limit - 1, kinds_mask & 3u));
+    }
+    std::vector<bnx_pair_t> rows;
+    for (int i = 0; i < ndev; ++i) {
+        std::vector<bnx_pair_t> part;
+        TRY(activate(g_multi[i]));
+        TRY(collect(g_multi[i], part));
+        rows.insert(rows.end(), part.begin(), part.end());
+    }
     std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
         return a.m != b.m ? a.m < b.m : a.n < b.n;
     });

@@ -58,3 +58,12 @@ def find_pairs(limit: int, *, kinds=None, primes: PrimeList | None = None,
 def last_stats(device: int | None = None) -> dict:
     """Counters of the last search on `device` (survivors, candidates, matches, ...)."""
     return _native.context(device).stats()
+
+
+def find_pairs_multi_gpu(limit: int, devices, *, kinds=None, primes: PrimeList | None = None) -> list[BeneluxPair]:
+    """Every pair m < n < limit on several GPUs driven from this thread (bnx_search_multi):
+    device i computes shard i of len(devices); the merged list equals find_pairs(limit)."""
+    if limit < 3:
+        raise ValueError("limit must be >= 3")
+    p, lim = _prime_args(primes)
+    return pairs_from_rows(_native.search_multi(list(devices), limit, kinds_mask(kinds), p, lim))

@@ -49,3 +49,17 @@ def test_multi_rank_device_search(world, golden):
     want = [tuple(r) for r in golden["find_pairs_sorted"][str(limit)]]
     for r in range(world):
         assert results[r] == want
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0, 0, 0]])
+def test_single_thread_multi_device_search(devices, golden):
+    """bnx_search_multi (one host thread drives the GPUs): shard i on
+    devices[i]; here every shard shares cuda:0.  Rows equal the single-device search and the
+    reference's list, for any number of shards."""
+    import paper_2506_01099_b200 as bp
+
+    limit = 1 << 24
+    got = [(int(p.kind), p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in bp.find_pairs_multi_gpu(limit, devices)]
+    assert got == [tuple(r) for r in golden["find_pairs_sorted"][str(limit)]]
+    big = bp.find_pairs_multi_gpu(1 << 36, devices)
+    assert [(p.m, p.n, p.kind) for p in big] == [(p.m, p.n, p.kind) for p in bp.find_pairs(1 << 36)]
