@@ -259,22 +259,6 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) 
     }
 }
 
-// Inverse of a modulo p (0 < a < p, p prime), extended Euclid in 32 bits.
-__device__ __forceinline__ uint32_t inv_mod_u32(uint32_t a, uint32_t p) {
-    int32_t t = 0, nt = 1;
-    uint32_t r = p, nr = a;
-    while (nr) {
-        const uint32_t q = r / nr;
-        const int32_t tt = t - (int32_t)q * nt;
-        t = nt;
-        nt = tt;
-        const uint32_t rr = r - q * nr;
-        r = nr;
-        nr = rr;
-    }
-    return (uint32_t)(t < 0 ? t + (int32_t)p : t);
-}
-
 // Classes with many k: y = k b -+ 1 runs through an arithmetic progression in k, so for an
 // odd prime p not dividing b, p | k b + 1 <=> k = -b^-1 and p | k b - 1 <=> k = +b^-1 (mod p).
 // Each CTA owns a contiguous run of chunks (up to kc consecutive k of one class each):
