@@ -9,19 +9,23 @@
 // b = sigma * rad(sigma) runs over the powerful numbers (b = prod p^(e+1) <-> sigma =
 // prod p^e), so the host lists the classes (b, sigma) once per bound (a DFS over primes) and
 // the device walks every (class, k) of the domain:
-//   k_heavy_count   per class: the k range that lands in the domain
-//   (cub scan)      flattened item offsets
+//   k_heavy_count   per class: the k range that lands in the domain; classes with many k
+//                   are counted in sieve chunks, the others in single items (one packed scan)
+//   (cub scan)      flattened item / chunk offsets
 //   k_heavy_screen  per item: canonical k (squarefree, coprime to sigma: bit tables), then
 //                   for y = x - 1 and y = x + 1 a conservative test of s(x) s(y) >= (n+1)/2:
 //                   y is trial-divided by the primes <= P2 = y_max^(1/4) only; the cofactor
 //                   c then has at most three prime factors, all > P2, so s(c) is 1, p (c = p^2
 //                   or p^2 q, p <= sqrt(c / (P2+1))) or p^2 (c = p^3) and is bounded exactly
+//   k_heavy_sieve   the same test for the classes with many k, with the trial division
+//                   replaced by sieving the progressions k = -+b^-1 (mod p) over a chunk of k
 //   k_heavy_exact   per survivor: rad(y) exactly (trial division to cbrt, cofactor 1, p,
 //                   p^2 or pq), the exact test R <= 2n, and de-duplication (a candidate with
 //                   both sides heavy is kept only from x = n)
 // The survivors of k_heavy_exact are exactly the candidates, with rad(n), rad(n+1) attached;
-// k_tail then walks their residue classes (bnx_kernels.cu).  Work: ~1.2M canonical heavy x
-// below 2^32 (instead of 2^32 integers), each costing ~54 trial divisions per side.
+// k_tail / k_tail_heavy then walk their residue classes (bnx_kernels.cu).  Work: ~1.2M
+// canonical heavy x below 2^32 (instead of 2^32 integers), each costing ~54 trial divisions
+// per side.  Every kernel here can run one shard of a search (HeavyArgs::shard, multi-GPU).
 #include <cub/device/device_scan.cuh>
 
 #include "bnx_kernels.cuh"
