@@ -390,7 +390,9 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
 // (the largest k any class can use: k^2 <= 2m * max_x / (m r^2) <= max_x / 2 for r >= 2).
 int build_heavy(bnx_ctx* c, uint64_t max_x) {
     HeavyTab& h = c->heavy_tab;
-    if (h.gen == c->gen && h.max_x >= max_x) return BNX_OK;
+    // a table for a larger bound serves (its extra classes count zero items), unless it is so
+    // much larger that the per-search class pass would dominate: then rebuild for this bound
+    if (h.gen == c->gen && h.max_x >= max_x && h.max_x / 16 <= max_x) return BNX_OK;
     const std::vector<uint32_t>& P = c->h_primes;
     const uint64_t root = isqrt_u64(max_x);
     if (P.empty() || (P.back() < root && c->primes_limit < root))
@@ -572,7 +574,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.shard = c->shard;
     ha.nshards = c->nshards;
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
-    launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * 8, c->stream, c->timing ? c->ev[1] : nullptr);
+    launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * 8, c->stream, c->timing ? c->ev[1] : nullptr, c->aux,
+                 c->fork_ev, c->join_ev);
     TailArgs ta{nullptr, 0, c->cand.p, c->cand.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p,
                 c->pairs.cap, c->ctr.p};
     // k_tail_heavy (the few candidates with many residue-class members) overlaps k_tail

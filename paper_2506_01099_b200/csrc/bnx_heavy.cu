@@ -533,23 +533,28 @@ size_t heavy_scan_temp_bytes(uint64_t nent) {
 }
 
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
-                  cudaEvent_t ev_generated) {
+                  cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     if (a.nent) {
         const unsigned cb = (unsigned)std::min<uint64_t>((a.nent + 255) / 256, 4096);
         k_heavy_count<<<cb, 256, 0, st>>>(a);
         size_t bytes = scan_temp_bytes;
         cub::DeviceScan::InclusiveSum(scan_temp, bytes, a.cnt, a.incl, (int64_t)a.nent, st);
-        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
-        k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
-        if (a.kmin != ~0ull) {
+        const bool sieve = a.kmin != ~0ull;
+        if (sieve) {  // the sieve (shared-memory atomics) runs beside the trial screen (IMAD pipe)
+            cudaEventRecord(ev_fork, st);
+            cudaStreamWaitEvent(aux, ev_fork, 0);
             const size_t smemS = heavy_sieve_smem(a.np2, a.kc, a.ntasks);
             static size_t attr_set = 0;
             if (smemS > 48 * 1024 && smemS > attr_set) {
                 cudaFuncSetAttribute(k_heavy_sieve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemS);
                 attr_set = smemS;
             }
-            k_heavy_sieve<<<grid, 256, smemS, st>>>(a);
+            k_heavy_sieve<<<grid, 256, smemS, aux>>>(a);
+            cudaEventRecord(ev_join, aux);
         }
+        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
+        k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
+        if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
     }
     const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
     static size_t attr3 = 0;

@@ -107,7 +107,7 @@ struct HeavyArgs {
 size_t heavy_scan_temp_bytes(uint64_t nent);
 size_t heavy_sieve_smem(int np2, int kc, int ntasks);
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
-                  cudaEvent_t ev_generated);
+                  cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join);
 
 struct SieveArgs {
     uint64_t start, length;
