@@ -574,7 +574,11 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.shard = c->shard;
     ha.nshards = c->nshards;
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
-    launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * 8, c->stream, c->timing ? c->ev[1] : nullptr, c->aux,
+    // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
+    // (6 resident CTAs per SM) below ~2^33; more, smaller runs when the sieve shares the GPU
+    const char* genv = std::getenv("BNX_HEAVY_GRID");  // tuning only
+    const int grid_mult = genv ? std::max(1, std::atoi(genv)) : (ha.kmin == ~0ull ? 6 : 20);
+    launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * grid_mult, c->stream, c->timing ? c->ev[1] : nullptr, c->aux,
                  c->fork_ev, c->join_ev);
     TailArgs ta{nullptr, 0, c->cand.p, c->cand.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p,
                 c->pairs.cap, c->ctr.p};
