@@ -140,6 +140,11 @@ struct bnx_ctx {
     bool own_stream = false;
     cudaStream_t aux = nullptr;  // second stream: k_tail_heavy beside k_tail (heavy engine)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // the heavy engine's search as a CUDA graph, re-captured whenever its parameters change
+    bool use_graphs = true;
+    cudaGraph_t graph = nullptr, graph2 = nullptr;
+    cudaGraphExec_t graph_exec = nullptr, graph_exec2 = nullptr;
+    std::vector<unsigned char> graph_key;
     int num_sms = 148;
     int screen_blocks_per_sm = 1;
     int screen_v = 0;
@@ -527,9 +532,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         h.tasks_np2 = (int)np2;
         h.tasks_kc = kc;
     }
-    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
-    CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
-    HeavyArgs ha{};
+    HeavyArgs ha;
+    std::memset(&ha, 0, sizeof(ha));  // (the graph key compares bytes, padding included)
     ha.kcnt = h.kcnt.p;
     ha.tasks = h.tasks.p;
     ha.ntasks = h.ntasks;
@@ -573,26 +577,85 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.flags = c->flags.p;
     ha.shard = c->shard;
     ha.nshards = c->nshards;
-    if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
     // (6 resident CTAs per SM) below ~2^33; more, smaller runs when the sieve shares the GPU
     const char* genv = std::getenv("BNX_HEAVY_GRID");  // tuning only
     const int grid_mult = genv ? std::max(1, std::atoi(genv)) : (ha.kmin == ~0ull ? 6 : 20);
-    launch_heavy(ha, h.scan_temp.p, h.scan_bytes, c->num_sms * grid_mult, c->stream, c->timing ? c->ev[1] : nullptr, c->aux,
-                 c->fork_ev, c->join_ev);
-    TailArgs ta{nullptr, 0, c->cand.p, c->cand.cap, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p,
-                c->pairs.cap, c->ctr.p};
-    // k_tail_heavy (the few candidates with many residue-class members) overlaps k_tail
-    CK(cudaEventRecord(c->fork_ev, c->stream));
-    CK(cudaStreamWaitEvent(c->aux, c->fork_ev, 0));
-    launch_tail_heavy(ta, c->aux);
-    CK(cudaEventRecord(c->join_ev, c->aux));
-    launch_tail_light(ta, grid_for(c), c->stream);
-    CK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
-    CK(cudaGetLastError());
-    if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
-    CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    const int grid = c->num_sms * grid_mult;
+    TailArgs ta;
+    std::memset(&ta, 0, sizeof(ta));
+    ta.cands = c->cand.p;
+    ta.cand_cap = c->cand.cap;
+    ta.heavy = c->heavy.p;
+    ta.heavy_cap = c->heavy.cap;
+    ta.pdiv = t.pdiv.p;
+    ta.npdiv = t.npdiv;
+    ta.kinds = kinds;
+    ta.pairs = c->pairs.p;
+    ta.pair_cap = c->pairs.cap;
+    ta.ctr = c->ctr.p;
+    // two phases (generator; tail + read-back), so the timing events sit between them
+    auto record_gen = [&]() -> int {
+        CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+        CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+        launch_heavy(ha, h.scan_temp.p, h.scan_bytes, grid, c->stream, nullptr, c->aux, c->fork_ev, c->join_ev);
+        CK(cudaGetLastError());
+        return BNX_OK;
+    };
+    auto record_tail = [&]() -> int {
+        // k_tail_heavy (the few candidates with many residue-class members) overlaps k_tail
+        CK(cudaEventRecord(c->fork_ev, c->stream));
+        CK(cudaStreamWaitEvent(c->aux, c->fork_ev, 0));
+        launch_tail_heavy(ta, c->aux);
+        CK(cudaEventRecord(c->join_ev, c->aux));
+        launch_tail_light(ta, grid_for(c), c->stream);
+        CK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+        return BNX_OK;
+    };
+    if (!c->use_graphs) {
+        if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
+        TRY(record_gen());
+        if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
+        TRY(record_tail());
+        if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+    } else {
+        // two graph launches replay the whole search (about ten stream operations): the host
+        // enqueue cost and the inter-kernel gaps go; re-captured when any parameter changes
+        std::vector<unsigned char> key(sizeof(ha) + sizeof(ta) + 3 * sizeof(uint64_t));
+        unsigned char* kp = key.data();
+        std::memcpy(kp, &ha, sizeof(ha));
+        std::memcpy(kp + sizeof(ha), &ta, sizeof(ta));
+        const uint64_t extra[3] = {(uint64_t)(uintptr_t)c->stream, (uint64_t)grid,
+                                   (uint64_t)(uintptr_t)h.scan_temp.p ^ (uint64_t)h.scan_bytes << 1};
+        std::memcpy(kp + sizeof(ha) + sizeof(ta), extra, sizeof(extra));
+        if (!c->graph_exec || !c->graph_exec2 || key != c->graph_key) {
+            for (auto* ge : {&c->graph_exec, &c->graph_exec2})
+                if (*ge) cudaGraphExecDestroy(*ge), *ge = nullptr;
+            for (auto* g : {&c->graph, &c->graph2})
+                if (*g) cudaGraphDestroy(*g), *g = nullptr;
+            c->graph_key.clear();
+            auto capture = [&](auto&& fn, cudaGraph_t* g, cudaGraphExec_t* ge) -> int {
+                CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+                const int rc = fn();
+                const cudaError_t ec = cudaStreamEndCapture(c->stream, g);
+                if (rc != BNX_OK) return rc;
+                if (ec != cudaSuccess) return fail(BNX_ERR_CUDA, std::string("stream capture: ") + cudaGetErrorString(ec));
+                CK(cudaGraphInstantiate(ge, *g, 0));
+                return BNX_OK;
+            };
+            TRY(capture(record_gen, &c->graph, &c->graph_exec));
+            TRY(capture(record_tail, &c->graph2, &c->graph_exec2));
+            c->graph_key = key;
+        }
+        if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
+        CK(cudaGraphLaunch(c->graph_exec, c->stream));
+        if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
+        CK(cudaGraphLaunch(c->graph_exec2, c->stream));
+        if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+    }
     c->q_valid = true;
     c->q_first = n_first;
     c->q_last = n_last;
@@ -776,6 +839,8 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    CK(heavy_configure());
+    if (const char* env = std::getenv("BNX_GRAPHS")) c->use_graphs = std::atoi(env) != 0;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
@@ -825,6 +890,10 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    if (c->graph_exec2) cudaGraphExecDestroy(c->graph_exec2);
+    if (c->graph) cudaGraphDestroy(c->graph);
+    if (c->graph2) cudaGraphDestroy(c->graph2);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     if (c->join_ev) cudaEventDestroy(c->join_ev);

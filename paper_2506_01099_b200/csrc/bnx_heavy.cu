@@ -526,6 +526,17 @@ size_t heavy_sieve_smem(int np2, int kc, int ntasks) {
            sizeof(uint32_t) * ((size_t)ntasks + kc);
 }
 
+// Dynamic shared memory limits of the heavy kernels, set once per device (outside any
+// stream capture): the sieve's masks and the exact stage's prime table can exceed 48 KB.
+cudaError_t heavy_configure() {
+    cudaError_t e = cudaFuncSetAttribute(k_heavy_sieve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_heavy_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    return e;
+}
+
 size_t heavy_scan_temp_bytes(uint64_t nent) {
     size_t bytes = 0;
     cub::DeviceScan::InclusiveSum(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)nent);
@@ -544,11 +555,6 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
             cudaEventRecord(ev_fork, st);
             cudaStreamWaitEvent(aux, ev_fork, 0);
             const size_t smemS = heavy_sieve_smem(a.np2, a.kc, a.ntasks);
-            static size_t attr_set = 0;
-            if (smemS > 48 * 1024 && smemS > attr_set) {
-                cudaFuncSetAttribute(k_heavy_sieve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemS);
-                attr_set = smemS;
-            }
             k_heavy_sieve<<<grid, 256, smemS, aux>>>(a);
             cudaEventRecord(ev_join, aux);
         }
@@ -557,11 +563,6 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
     }
     const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
-    static size_t attr3 = 0;
-    if (smem3 > 48 * 1024 && smem3 > attr3) {
-        cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
-        attr3 = smem3;
-    }
     k_heavy_exact<<<grid, 256, smem3, st>>>(a);
     if (ev_generated) cudaEventRecord(ev_generated, st);
 }

@@ -105,6 +105,7 @@ struct HeavyArgs {
     uint32_t shard, nshards;  // this search covers items/chunks [shard, shard + 1) / nshards
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
+cudaError_t heavy_configure();
 size_t heavy_sieve_smem(int np2, int kc, int ntasks);
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
                   cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join);
