@@ -578,9 +578,10 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.shard = c->shard;
     ha.nshards = c->nshards;
     // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
-    // (6 resident CTAs per SM) below ~2^33; more, smaller runs when the sieve shares the GPU
+    // (8 resident CTAs per SM at 32 registers) below ~2^33; more, smaller runs when the sieve
+    // shares the GPU
     const char* genv = std::getenv("BNX_HEAVY_GRID");  // tuning only
-    const int grid_mult = genv ? std::max(1, std::atoi(genv)) : (ha.kmin == ~0ull ? 6 : 20);
+    const int grid_mult = genv ? std::max(1, std::atoi(genv)) : (ha.kmin == ~0ull ? 8 : 20);
     const int grid = c->num_sms * grid_mult;
     TailArgs ta;
     std::memset(&ta, 0, sizeof(ta));

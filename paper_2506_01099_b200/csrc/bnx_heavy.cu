@@ -200,7 +200,7 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
 // takes item base + t: neighbouring k of one class, or neighbouring classes).  Canonical
 // items go to a shared-memory queue; whenever it holds a full CTA's worth, every thread
 // takes one and runs the y tests, so the expensive part always runs with full warps.
-__global__ void __launch_bounds__(HEAVY_THREADS, 6) k_heavy_screen(HeavyArgs a) {
+__global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) {
     constexpr int T = HEAVY_THREADS;
     extern __shared__ ulonglong2 s_il[];  // np2 (inv, lim), np2 (inv32, lim32), np2 p
     uint2* s_pd32 = reinterpret_cast<uint2*>(s_il + a.np2);
