@@ -31,7 +31,7 @@
  *                               (radical.py:119-120)
  *   BNX_ERR_INVALID          4  bad argument (limit < 3, empty interval, ...) -> ValueError
  *   BNX_ERR_CUDA             5  CUDA runtime failure / no device           -> RuntimeError
- *   BNX_ERR_RANGE            6  bound beyond this build's exact range (S > 2^44; S >= 2^42
+ *   BNX_ERR_RANGE            6  bound beyond this build's exact range (S > 2^48; S >= 2^42
  *                                with the byte-screen engine)
  *   bnx_last_error() gives a message for the most recent failure on the calling thread.
  */

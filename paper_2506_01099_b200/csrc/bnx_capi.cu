@@ -738,8 +738,8 @@ int empty_search(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) 
 
 int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint64_t plimit) {
     // heavy generator: 64-bit arithmetic with margin and its shared-memory prime tables up to
-    // S = 2^44; the byte screen's 7-bit surplus weights up to S < 2^42
-    if (c->engine == 0 && max_x > (1ull << 44)) return fail(BNX_ERR_RANGE, "search bound must be at most 2^44");
+    // S = 2^48; the byte screen's 7-bit surplus weights up to S < 2^42
+    if (c->engine == 0 && max_x > (1ull << 48)) return fail(BNX_ERR_RANGE, "search bound must be at most 2^48");
     if (c->engine != 0 && max_x >= (1ull << 42))
         return fail(BNX_ERR_RANGE, "search bound must be below 2^42 with the byte-screen engine");
     const uint64_t need = isqrt_u64(max_x);

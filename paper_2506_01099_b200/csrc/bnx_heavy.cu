@@ -48,19 +48,26 @@ __device__ __forceinline__ uint32_t gcd32(uint32_t a, uint32_t b) {
     return a << sh;
 }
 
+// Exact integer square root test: q with q^2 = c, or 0.  A float root, rounded, is within
+// 0.4 of the integer one for c < 2^45; above, a double root (exact to 2^52).
+__device__ __forceinline__ uint64_t exact_sqrt(uint64_t c) {
+    const uint64_t q = c < (1ull << 45) ? (uint64_t)rintf(sqrtf((float)c)) : (uint64_t)llrint(sqrt((double)c));
+    return q * q == c ? q : 0;
+}
+
 // Upper bound of s(c) for an odd cofactor c > 0 whose prime factors all exceed P2 (p1 =
 // P2 + 1, p1^4 > c): c is 1, p, pq, pqr (s = 1), p^2 (s = sqrt c), p^2 q (s = p <=
 // sqrt(c / p1)) or p^3 (s = c^(2/3)).  Only an upper bound is needed (k_heavy_exact
 // decides), so the p^2 q case uses a rounded-up float root; squares and cubes are detected
-// exactly (float root, rounded, checked in integers; c < 2^45 keeps the float root within
-// 0.25 of the integer one).
+// exactly (rounded roots checked in integers, see exact_sqrt; the cube root of c < 2^50 is
+// below 2^17, where cbrtf's error is < 0.02).
 __device__ __forceinline__ uint64_t surplus_bound(uint64_t c, const HeavyArgs& a) {
     if (c < a.p1sq) return 1;  // 1 or a prime
     uint64_t u = 1;
     const float cf = (float)c;
     if ((c & 7) == 1) {  // odd squares are 1 mod 8
-        const uint64_t q = (uint64_t)rintf(sqrtf(cf));
-        if (q * q == c) u = q;
+        const uint64_t q = exact_sqrt(c);
+        if (q) u = q;
     }
     if (c >= a.p1cube) {
         const uint64_t v = (uint64_t)(sqrtf(cf * a.inv_p1f) * 1.0001f) + 1;  // >= sqrt(c / p1)
@@ -506,8 +513,8 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
             }
         }
         if (c > 1) {  // at most two primes > cbrt(y) remain: c = p, p^2 or pq
-            const uint64_t q = (uint64_t)rintf(sqrtf((float)c));  // exact for c < 2^45 (see surplus_bound)
-            rady *= (q * q == c) ? q : c;
+            const uint64_t q = exact_sqrt(c);
+            rady *= q ? q : c;
         }
         if (__umul64hi(radx, rady) != 0 || radx * rady > 2 * n) continue;
         if (sideL) {  // keep from x = n + 1 only if n itself is not heavy

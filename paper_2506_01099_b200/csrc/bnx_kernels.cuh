@@ -62,8 +62,8 @@ struct TailArgs {
 
 // Heavy-side generator (bnx_heavy.cu).
 constexpr int HEAVY_THREADS = 256;
-constexpr int HEAVY_NP2 = 512;   // odd primes <= y_max^(1/4) staged in shared memory
-constexpr int HEAVY_NP3 = 4096;  // odd primes <= cbrt(y_max) staged in shared memory (S <= 2^44)
+constexpr int HEAVY_NP2 = 1023;  // odd primes <= y_max^(1/4) staged in shared memory (10-bit task index)
+constexpr int HEAVY_NP3 = 7000;  // odd primes <= cbrt(y_max) staged in shared memory (S <= 2^48)
 // Classes with at least HEAVY_KMIN values of k in a domain are sieved over k (k_heavy_sieve)
 // in chunks of up to kc values; the rest go through trial division (k_heavy_screen).  Item
 // counts are packed: low 40 bits trial items, high 24 bits sieve chunks (one scan).

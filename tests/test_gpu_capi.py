@@ -39,7 +39,7 @@ def test_error_codes(L, ctx):
     buf = (_native.PairRow * 4)()
     assert L.bnx_search(ctx, 2, 3, None, 0, 0, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_INVALID
     assert L.bnx_search(ctx, 100, 0, None, 0, 0, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_INVALID
-    assert L.bnx_search(ctx, (1 << 44) + 1, 3, None, 0, 0, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_RANGE
+    assert L.bnx_search(ctx, (1 << 48) + 1, 3, None, 0, 0, buf, 4, ctypes.byref(found)) == _native.BNX_ERR_RANGE
     assert L.bnx_ctx_set_shard(ctx, 2, 2) == _native.BNX_ERR_INVALID
     assert L.bnx_ctx_set_shard(ctx, 0, 0) == _native.BNX_ERR_INVALID
     primes = np.array([2, 3, 5, 7], np.uint64)

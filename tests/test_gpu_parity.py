@@ -235,11 +235,11 @@ def test_heavy_candidates_on_random_domains(orc):
 
 
 def test_heavy_candidates_beyond_the_paper(orc):
-    """Windows between 2^42 and 2^44 (beyond the byte screen's range and the paper's 1.4e12):
+    """Windows between 2^42 and 2^48 (beyond the byte screen's range and the paper's 1.4e12):
     the heavy generator's exact candidate count equals the oracle's sieve count."""
     rng = np.random.default_rng(9)
-    for _ in range(4):
-        lo = int(rng.integers(2**42, 2**44 - 2**22))
+    for top in (44, 46, 48):
+        lo = int(rng.integers(2**(top - 2), 2**top - 2**22))
         hi = lo + (1 << 21)
         bp.search_domain(lo, hi)
         assert bp.last_stats()["candidates"] == exact_candidates(orc, lo, hi), (lo, hi)
@@ -278,9 +278,9 @@ def test_random_domains_vs_oracle(orc):
 
 def test_near_the_top_of_the_range():
     """Largest supported bounds: the first-kind family member (2^k - 2, 2^(2k) - 2^(k+1)) just
-    below the top must be found with its radicals -- k = 22 below 2^44 with the heavy
+    below the top must be found with its radicals -- k = 24 below 2^48 with the heavy
     generator, k = 21 below 2^42 with the byte screen -- and larger bounds are refused."""
-    for name, k, top in (("heavy", 22, 2**44), ("screen", 21, 2**42)):
+    for name, k, top in (("heavy", 24, 2**48), ("screen", 21, 2**42)):
         with engine(name):
             m, n = 2**k - 2, 2**(2 * k) - 2**(k + 1)
             got = bp.search_domain(n - 5000, n + 5000)
