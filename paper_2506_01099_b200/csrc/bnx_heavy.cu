@@ -223,10 +223,11 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     }
     if (tid == 0) s_cnt = 0;
     if (a.nent == 0) return;
-    // this shard's share of the trial items (multi-GPU: every rank walks 1/nshards of them)
+    // the trial items in gridDim * nshards equal runs; CTA g of shard s takes run g * nshards + s,
+    // so every shard samples the whole class range (the classes differ in canonical density)
     const uint64_t Wt = a.incl[a.nent - 1] & HEAVY_TRIAL_MASK;
-    const uint64_t s0 = Wt * a.shard / a.nshards, W = Wt * (a.shard + 1) / a.nshards - s0;
-    const uint64_t b0 = s0 + W * blockIdx.x / gridDim.x, b1 = s0 + W * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t nb = (uint64_t)gridDim.x * a.nshards, blk = (uint64_t)blockIdx.x * a.nshards + a.shard;
+    const uint64_t b0 = Wt * blk / nb, b1 = Wt * (blk + 1) / nb;
     if (tid == 0 && b0 < b1) s_cls = first_class_above(a.incl, 0, a.nent, b0);
     __syncthreads();
     uint64_t base = b0;
@@ -310,9 +311,9 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
     }
     for (int t = tid; t < a.ntasks; t += blockDim.x) s_task[t] = a.tasks[t];
     if (a.nent == 0) return;
-    const uint64_t Ct = a.incl[a.nent - 1] >> 40;  // this shard's share of the chunks
-    const uint64_t q0 = Ct * a.shard / a.nshards, C = Ct * (a.shard + 1) / a.nshards - q0;
-    const uint64_t c_begin = q0 + C * blockIdx.x / gridDim.x, c_end = q0 + C * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t Ct = a.incl[a.nent - 1] >> 40;  // runs of chunks interleaved over the shards (as above)
+    const uint64_t nb = (uint64_t)gridDim.x * a.nshards, blk = (uint64_t)blockIdx.x * a.nshards + a.shard;
+    const uint64_t c_begin = Ct * blk / nb, c_end = Ct * (blk + 1) / nb;
     for (uint64_t ch = c_begin; ch < c_end; ++ch) {
         __syncthreads();
         if (tid == 0) {
