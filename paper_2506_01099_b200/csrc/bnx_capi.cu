@@ -501,7 +501,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // k_heavy_sieve: chunk length (masks of 32 primes per word, ~32 KB of shared memory) and
     // the marking tasks: prime j, side, sub-progression r of R, about HEAVY_TASK_HITS hits each
     const int W = (int)((np2 + 31) / 32);
-    const int kc = std::max(32, std::min(4096, (6144 / std::max(W, 1)) & ~31));
+    (void)W;
+    const int kc = 1536;  // hit lists: 2 x kc x (8 slots x 2 B + 1 B) = 51 KB of shared memory
     if (h.tasks_np2 != (int)np2 || h.tasks_kc != kc) {
         std::vector<uint32_t> tk, ioff;
         std::vector<uint16_t> itab;

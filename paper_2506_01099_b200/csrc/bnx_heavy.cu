@@ -273,17 +273,19 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
 
 // Classes with many k: y = k b -+ 1 runs through an arithmetic progression in k, so for an
 // odd prime p not dividing b, p | k b + 1 <=> k = -b^-1 and p | k b - 1 <=> k = +b^-1 (mod p).
-// Each CTA owns a contiguous run of chunks (up to kc consecutive k of one class each):
+// Each CTA owns runs of chunks (up to kc consecutive k of one class each):
 //   1. per prime <= P2, on entering a class: b mod p (Barrett with the table's
 //      floor((2^64-1)/p)), b^-1 mod p (host table), the first index of each side's
 //      progression in the chunk; for the next chunk of the same class the indices just
 //      move by kc mod p;
-//   2. marks: host-built tasks of ~16 hits each set bit j of word j/32 of the k's mask
-//      (shared atomicOr; one mask per side and 32 primes);
+//   2. marks: host-built tasks of ~16 hits each append the prime's index to the (k, side)
+//      hit list in shared memory (a packed byte counter per list, HEAVY_HITS slots; a list
+//      that overflows is redone by trial division in step 4);
 //   3. canonical k of the chunk are compacted into a shared list;
-//   4. per canonical k: the marked primes are divided out of both y exactly (with their
+//   4. per canonical k: the listed primes are divided out of both y exactly (with their
 //      powers) and the same stage-1 test as k_heavy_screen decides.
-// So the per-k work is ~3 marks and ~3 exact divisions instead of 2 pi(P2) trial divisions.
+// So the per-k work is ~3 marks and ~3 exact divisions instead of 2 pi(P2) trial divisions,
+// and it does not grow with pi(P2).
 __device__ __forceinline__ uint64_t mod_by_lim(uint64_t v, uint64_t p, uint64_t lim) {
     uint64_t r = v - __umul64hi(v, lim) * p;  // lim = floor((2^64-1)/p): quotient off by <= 1
     while (r >= p) r -= p;
@@ -292,14 +294,15 @@ __device__ __forceinline__ uint64_t mod_by_lim(uint64_t v, uint64_t p, uint64_t 
 
 __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
-    const int np2 = a.np2, kc = a.kc, W = (np2 + 31) >> 5;
-    uint32_t* masks = reinterpret_cast<uint32_t*>(sm_raw);               // [2][W][kc]
-    ulonglong2* s_il = reinterpret_cast<ulonglong2*>(masks + 2 * W * kc);  // np2
-    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + np2);                // np2
-    int32_t* s_off = reinterpret_cast<int32_t*>(s_p + np2);                 // 2 np2
-    uint32_t* s_kcm = reinterpret_cast<uint32_t*>(s_off + 2 * np2);         // np2: kc mod p
-    uint32_t* s_task = s_kcm + np2;                                         // ntasks
-    uint32_t* s_list = s_task + a.ntasks;                                   // kc
+    const int np2 = a.np2, kc = a.kc;
+    uint16_t* hits = reinterpret_cast<uint16_t*>(sm_raw);                      // [2][kc][HEAVY_HITS]
+    uint32_t* hcnt = reinterpret_cast<uint32_t*>(hits + 2 * kc * HEAVY_HITS);  // [2][kc / 4] packed bytes
+    ulonglong2* s_il = reinterpret_cast<ulonglong2*>(hcnt + kc / 2);          // np2
+    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + np2);                   // np2
+    int32_t* s_off = reinterpret_cast<int32_t*>(s_p + np2);                    // 2 np2
+    uint32_t* s_kcm = reinterpret_cast<uint32_t*>(s_off + 2 * np2);            // np2: kc mod p
+    uint32_t* s_task = s_kcm + np2;                                            // ntasks
+    uint32_t* s_list = s_task + a.ntasks;                                      // kc
     __shared__ BnxHeavyEnt s_e;
     __shared__ uint64_t s_k0, s_kend, s_cls_end;
     __shared__ int s_nl, s_fresh;
@@ -360,9 +363,9 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                 s_off[2 * j + 1] = (int32_t)(((uint32_t)s_off[2 * j + 1] + d) % p);
             }
         }
-        for (int w = tid; w < (2 * W * kc) >> 2; w += blockDim.x) reinterpret_cast<uint4*>(masks)[w] = make_uint4(0, 0, 0, 0);
+        for (int w = tid; w < kc / 2; w += blockDim.x) hcnt[w] = 0;
         __syncthreads();
-        // 2. marks
+        // 2. marks: append j to the hit list of (k, side)
         for (int t = tid; t < a.ntasks; t += blockDim.x) {
             const uint32_t tk = s_task[t];
             const int j = tk & 0x3FF, side = (tk >> 10) & 1;
@@ -370,9 +373,12 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
             const int32_t off = s_off[2 * j + side];
             if (off < 0) continue;
             const uint32_t p = s_p[j];
-            uint32_t* m = masks + (side * W + (j >> 5)) * kc;
-            const uint32_t bit = 1u << (j & 31);
-            for (uint32_t kk = (uint32_t)off + r * p; kk < (uint32_t)kn; kk += R * p) atomicOr(&m[kk], bit);
+            for (uint32_t kk = (uint32_t)off + r * p; kk < (uint32_t)kn; kk += R * p) {
+                const uint32_t li = (uint32_t)side * kc + kk;
+                const uint32_t sh = 8 * (li & 3);
+                const uint32_t slot = (atomicAdd(&hcnt[li >> 2], 1u << sh) >> sh) & 0xFF;
+                if (slot < HEAVY_HITS) hits[li * HEAVY_HITS + slot] = (uint16_t)j;
+            }
         }
         // 3. canonical k of the chunk
         for (int kk = tid; kk < kn; kk += blockDim.x) {
@@ -400,14 +406,22 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                 const uint64_t y = side ? x - 1 : x + 1;
                 const int tz = __ffsll((long long)y) - 1;
                 uint64_t c = y >> tz, sy = tz ? 1ull << (tz - 1) : 1ull;
-                for (int w = 0; w < W; ++w) {
-                    uint32_t m = masks[(side * W + w) * kc + kk];
-                    while (m) {
-                        const int j = 32 * w + __ffs(m) - 1;
-                        m &= m - 1;
+                const uint32_t hl = (uint32_t)side * kc + kk;
+                const uint32_t nh = (hcnt[hl >> 2] >> (8 * (hl & 3))) & 0xFF;
+                if (nh <= (uint32_t)HEAVY_HITS) {
+                    for (uint32_t h = 0; h < nh; ++h) {
+                        const int j = hits[hl * HEAVY_HITS + h];
                         const ulonglong2 d = s_il[j];
                         c *= d.x;
                         while (c * d.x <= d.y) { c *= d.x; sy *= s_p[j]; }
+                    }
+                } else {  // more distinct small primes than slots (rare): trial division
+                    for (int j = 0; j < np2; ++j) {
+                        const ulonglong2 d = s_il[j];
+                        if (c * d.x <= d.y) {
+                            c *= d.x;
+                            while (c * d.x <= d.y) { c *= d.x; sy *= s_p[j]; }
+                        }
                     }
                 }
                 const bool pass = twice_prod_ge(sigma, sy * surplus_bound(c, a), side ? x : x + 1);
@@ -529,8 +543,8 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
 }  // namespace
 
 size_t heavy_sieve_smem(int np2, int kc, int ntasks) {
-    const int W = (np2 + 31) >> 5;
-    return sizeof(uint32_t) * (size_t)2 * W * kc + (sizeof(ulonglong2) + 2 * sizeof(uint32_t) + 2 * sizeof(int32_t)) * np2 +
+    return sizeof(uint16_t) * (size_t)2 * kc * HEAVY_HITS + (size_t)2 * kc +
+           (sizeof(ulonglong2) + 2 * sizeof(uint32_t) + 2 * sizeof(int32_t)) * np2 +
            sizeof(uint32_t) * ((size_t)ntasks + kc);
 }
 

@@ -70,6 +70,7 @@ constexpr int HEAVY_NP3 = 7000;  // odd primes <= cbrt(y_max) staged in shared m
 constexpr uint64_t HEAVY_KMIN_DEFAULT = 512;
 constexpr uint64_t HEAVY_TRIAL_MASK = (1ull << 40) - 1;
 constexpr int HEAVY_TASK_HITS = 16;  // marks per sieve task (host-built task list)
+constexpr int HEAVY_HITS = 8;        // hit-list slots per (k, side) in k_heavy_sieve (more: trial division)
 struct HeavyArgs {
     const BnxHeavyEnt* ent;
     uint64_t nent;
