@@ -138,7 +138,7 @@ struct HeavyItem {
 // The y tests of one heavy x (both sides), see the file comment.  Shared tables: (inv, lim)
 // and p of the odd primes <= P2.
 __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
-                                        const uint32_t* s_p, const uint2* s_pd32) {
+                                        const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32) {
     const uint64_t x = it.x;
     const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
     const bool vU = x >= a.n_first && x <= a.n_last;
@@ -151,8 +151,7 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
     // Both y below 2^32 (domains below 2^32): 32-bit tests, one IMAD per prime and side
     // instead of a 64-bit multiply (the kernel is IMAD-pipe bound).
     const bool narrow = yU < (1ull << 32);
-    const uint64_t oL = cL, oU = cU;
-    const uint32_t x32 = (uint32_t)x;
+    const uint32_t x32 = (uint32_t)x, xh = (uint32_t)(x >> 32);
     for (int j0 = 0; j0 < a.np2; j0 += 32) {
         const int jn = min(32, a.np2 - j0);
         uint32_t mL = 0, mU = 0;
@@ -167,12 +166,21 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
             }
             mL = vL ? mL : 0u;
         } else {
+            // x >= 2^32 (x < 2^53): w = x_lo + x_hi (2^32 mod p) is x mod p shifted into 32
+            // bits (a carry out of the add is 2^32 = 2^32 mod p); then the same test on w -+ 1.
+            // w - 1 and w + 1 can wrap at 0 and 2^32 - 1: such rare false bits are rejected by
+            // the exact division check below.
 #pragma unroll 8
             for (int u = 0; u < jn; ++u) {
-                const ulonglong2 d = s_il[j0 + u];
-                mL |= (uint32_t)(oL * d.x <= d.y) << u;
-                mU |= (uint32_t)(oU * d.x <= d.y) << u;
+                const uint2 d = s_pd32[j0 + u];
+                const uint32_t cp = s_c32[j0 + u];
+                uint32_t w = x32 + xh * cp;
+                if (w < x32) w += cp;
+                const uint32_t t = w * d.x;
+                mL |= (uint32_t)(t - d.x <= d.y) << u;
+                mU |= (uint32_t)(t + d.x <= d.y) << u;
             }
+            mL = vL ? mL : 0u;
         }
         while (mL | mU) {  // one hit of each side per round: the rounds are shared
             if (mL) {
@@ -180,16 +188,22 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
                 mL &= mL - 1;
                 const ulonglong2 d = s_il[j0 + u];
                 const uint64_t pp = s_p[j0 + u];
-                cL *= d.x;
-                while (cL * d.x <= d.y) { cL *= d.x; sL *= pp; }
+                uint64_t t = cL * d.x;
+                if (t <= d.y) {  // p | cL exactly (rejects a wrapped false bit)
+                    cL = t;
+                    for (t = cL * d.x; t <= d.y; t = cL * d.x) { cL = t; sL *= pp; }
+                }
             }
             if (mU) {
                 const int u = __ffs(mU) - 1;
                 mU &= mU - 1;
                 const ulonglong2 d = s_il[j0 + u];
                 const uint64_t pp = s_p[j0 + u];
-                cU *= d.x;
-                while (cU * d.x <= d.y) { cU *= d.x; sU *= pp; }
+                uint64_t t = cU * d.x;
+                if (t <= d.y) {
+                    cU = t;
+                    for (t = cU * d.x; t <= d.y; t = cU * d.x) { cU = t; sU *= pp; }
+                }
             }
         }
     }
@@ -209,9 +223,10 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
 // takes one and runs the y tests, so the expensive part always runs with full warps.
 __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) {
     constexpr int T = HEAVY_THREADS;
-    extern __shared__ ulonglong2 s_il[];  // np2 (inv, lim), np2 (inv32, lim32), np2 p
+    extern __shared__ ulonglong2 s_il[];  // np2 (inv, lim), np2 (inv32, lim32), np2 p, np2 2^32 mod p
     uint2* s_pd32 = reinterpret_cast<uint2*>(s_il + a.np2);
     uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + a.np2);
+    uint32_t* s_c32 = s_p + a.np2;
     __shared__ HeavyItem s_q[2 * T];
     __shared__ int s_cnt;
     __shared__ unsigned long long s_cls;
@@ -220,6 +235,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         s_il[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
         s_pd32[j] = make_uint2((uint32_t)a.pdiv[j].inv, 0xFFFFFFFFu / (uint32_t)a.pdiv[j].p);  // p^-1 mod 2^32
         s_p[j] = (uint32_t)a.pdiv[j].p;
+        s_c32[j] = (uint32_t)((1ull << 32) % a.pdiv[j].p);
     }
     if (tid == 0) s_cnt = 0;
     if (a.nent == 0) return;
@@ -263,7 +279,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         }
         if (cnt == 0) break;
         const int take = min(cnt, T);
-        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p, s_pd32);
+        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p, s_pd32, s_c32);
         cnt -= take;
         __syncthreads();
         if (tid == 0) s_cnt = cnt;
@@ -580,7 +596,7 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
             k_heavy_sieve<<<grid, 256, smemS, aux>>>(a);
             cudaEventRecord(ev_join, aux);
         }
-        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
+        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint2) + 2 * sizeof(uint32_t));
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
     }
