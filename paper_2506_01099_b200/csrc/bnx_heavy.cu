@@ -478,14 +478,16 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
 // from shared memory, 32 per bit mask as in y_tests; the cofactor is then 1, p, p^2 or pq),
 // the exact test R <= 2n, de-duplication, emission.
 __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
-    extern __shared__ ulonglong2 s_il3[];  // np3 (inv, lim), np3 (inv32, lim32), np3 p
+    extern __shared__ ulonglong2 s_il3[];  // np3 (inv, lim), np3 (inv32, lim32), np3 p, np3 2^32 mod p
     uint2* s_pd3 = reinterpret_cast<uint2*>(s_il3 + a.np3);
     uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_pd3 + a.np3);
+    uint32_t* s_c3 = s_p3 + a.np3;
     const int np3 = (int)a.np3;
     for (int j = threadIdx.x; j < np3; j += blockDim.x) {
         s_il3[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
         s_pd3[j] = make_uint2((uint32_t)a.pdiv[j].inv, 0xFFFFFFFFu / (uint32_t)a.pdiv[j].p);
         s_p3[j] = (uint32_t)a.pdiv[j].p;
+        s_c3[j] = (uint32_t)((1ull << 32) % a.pdiv[j].p);
     }
     __syncthreads();
     const uint64_t nq = min((uint64_t)a.ctr[CTR_SURV], a.q1_cap);
@@ -518,6 +520,7 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         const uint64_t o = y >> tz;
         uint64_t c = o, rady = tz ? 2 : 1;
         const bool narrow = o < (1ull << 32);  // 32-bit tests (see y_tests)
+        const uint32_t ol = (uint32_t)o, oh = (uint32_t)(o >> 32);
         for (int j0 = 0; j0 < np3; j0 += 32) {
             const int jn = min(32, np3 - j0);
             uint32_t m = 0;
@@ -527,11 +530,14 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
                     const uint2 d = s_pd3[j0 + u];
                     m |= (uint32_t)((uint32_t)o * d.x <= d.y) << u;
                 }
-            } else {
+            } else {  // o = oh 2^32 + ol: w = ol + oh (2^32 mod p) = o (mod p) in 32 bits (p, oh < 2^16)
 #pragma unroll 8
                 for (int u = 0; u < jn; ++u) {
-                    const ulonglong2 d = s_il3[j0 + u];
-                    m |= (uint32_t)(o * d.x <= d.y) << u;
+                    const uint2 d = s_pd3[j0 + u];
+                    const uint32_t cp = s_c3[j0 + u];
+                    uint32_t w = ol + oh * cp;
+                    if (w < ol) w += cp;
+                    m |= (uint32_t)(w * d.x <= d.y) << u;
                 }
             }
             while (m) {
@@ -569,7 +575,7 @@ size_t heavy_sieve_smem(int np2, int kc, int ntasks) {
 cudaError_t heavy_configure() {
     cudaError_t e = cudaFuncSetAttribute(k_heavy_sieve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_heavy_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     return e;
@@ -600,7 +606,7 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
     }
-    const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint2) + sizeof(uint32_t));
+    const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint2) + 2 * sizeof(uint32_t));
     k_heavy_exact<<<grid, 256, smem3, st>>>(a);
     if (ev_generated) cudaEventRecord(ev_generated, st);
 }
