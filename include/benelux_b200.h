@@ -82,7 +82,8 @@ typedef struct bnx_stats {
     uint64_t residue_checks; /* m values enumerated on the residue classes            */
     uint64_t matches;        /* (m, n) with equal signatures                          */
     uint64_t pairs;          /* rows emitted after the kind filter                    */
-    uint64_t kernel_launches;/* kernels this library launched for the call            */
+    uint64_t kernel_launches;/* this library's own kernels launched for the call (the   */
+                             /* cub scan of the heavy generator is not counted)         */
     int32_t bucket_overflow; /* nonzero if a tile bucket overflowed (call failed)     */
     int32_t reserved;
     uint64_t max_residue_checks; /* most residue-class members of a single candidate     */

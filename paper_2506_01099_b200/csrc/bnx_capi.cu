@@ -664,8 +664,9 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     c->q_kinds = kinds;
     c->stats = bnx_stats_t{};
     c->stats.integers = n_last - n_first + 1;
-    // count, scan (2), screen, [sieve], exact, tail, tail_heavy
-    c->stats.kernel_launches = ha.nent ? (ha.kmin != ~0ull ? 8 : 7) : 3;
+    // this library's kernels: count, screen, [sieve], exact, tail, tail_heavy (the two cub
+    // scan kernels are library code and not counted)
+    c->stats.kernel_launches = ha.nent ? (ha.kmin != ~0ull ? 6 : 5) : 3;
     return BNX_OK;
 }
 
