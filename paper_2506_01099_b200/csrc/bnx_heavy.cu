@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
     uint32_t* s_task = s_kcm + np2;                                            // ntasks
     uint32_t* s_list = s_task + a.ntasks;                                      // kc
     __shared__ BnxHeavyEnt s_e;
-    __shared__ uint64_t s_k0, s_kend, s_cls_end;
+    __shared__ uint64_t s_k0, s_kend, s_cls_end, s_cls;
     __shared__ int s_nl, s_fresh;
     const int tid = threadIdx.x;
     for (int j = tid; j < np2; j += blockDim.x) {
@@ -335,24 +335,41 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
     const uint64_t c_begin = Ct * blk / nb, c_end = Ct * (blk + 1) / nb;
     for (uint64_t ch = c_begin; ch < c_end; ++ch) {
         __syncthreads();
-        if (tid == 0) {
-            if (ch == c_begin || ch >= s_cls_end) {  // entering a class
-                uint64_t lo = 0, hi = a.nent - 1;      // first class with chunk prefix > ch
-                while (lo < hi) {
-                    const uint64_t mid = (lo + hi) >> 1;
-                    if ((a.incl[mid] >> 40) > ch) hi = mid; else lo = mid + 1;
+        if (tid < 32) {  // warp 0 finds the chunk's class
+            const bool enter = ch == c_begin || ch >= s_cls_end;
+            if (enter) {
+                uint64_t cls;
+                if (ch == c_begin) {  // first chunk of the run: binary search
+                    uint64_t lo = 0, hi = a.nent - 1;  // first class with chunk prefix > ch
+                    while (lo < hi) {
+                        const uint64_t mid = (lo + hi) >> 1;
+                        if ((a.incl[mid] >> 40) > ch) hi = mid; else lo = mid + 1;
+                    }
+                    cls = lo;
+                } else {  // the next sieve class: the 32 lanes probe the following classes
+                    uint64_t from = s_cls + 1;
+                    for (;;) {
+                        const uint64_t j = from + tid;
+                        const bool hit = j < a.nent && (a.incl[j] >> 40) > ch;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+                        if (bal) { cls = from + __ffs(bal) - 1; break; }
+                        from += 32;
+                    }
                 }
-                const uint64_t first = lo ? a.incl[lo - 1] >> 40 : 0;
-                s_e = a.ent[lo];
-                s_k0 = (uint64_t)a.klo[lo] + (ch - first) * (uint64_t)kc;
-                s_kend = (uint64_t)a.klo[lo] + a.kcnt[lo];
-                s_cls_end = a.incl[lo] >> 40;
-                s_fresh = 1;
-            } else {
+                if (tid == 0) {
+                    const uint64_t first = cls ? a.incl[cls - 1] >> 40 : 0;
+                    s_e = a.ent[cls];
+                    s_k0 = (uint64_t)a.klo[cls] + (ch - first) * (uint64_t)kc;
+                    s_kend = (uint64_t)a.klo[cls] + a.kcnt[cls];
+                    s_cls_end = a.incl[cls] >> 40;
+                    s_cls = cls;
+                    s_fresh = 1;
+                }
+            } else if (tid == 0) {
                 s_k0 += (uint64_t)kc;
                 s_fresh = 0;
             }
-            s_nl = 0;
+            if (tid == 0) s_nl = 0;
         }
         __syncthreads();
         const BnxHeavyEnt e = s_e;
