@@ -162,6 +162,7 @@ struct bnx_ctx {
     HeavyTab heavy_tab;
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
     uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
+    int heavy_grid = 0;       // tuning only (BNX_HEAVY_GRID, CTAs per SM); 0 = default
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
     DBuf<ulonglong2> q1;
     DBuf<BnxCand> cand;
@@ -581,8 +582,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
     // (8 resident CTAs per SM at 32 registers) below ~2^33; more, smaller runs when the sieve
     // shares the GPU
-    const char* genv = std::getenv("BNX_HEAVY_GRID");  // tuning only
-    const int grid_mult = genv ? std::max(1, std::atoi(genv)) : (ha.kmin == ~0ull ? 8 : 20);
+    const int grid_mult = c->heavy_grid ? c->heavy_grid : (ha.kmin == ~0ull ? 8 : 20);
     const int grid = c->num_sms * grid_mult;
     TailArgs ta;
     std::memset(&ta, 0, sizeof(ta));
@@ -848,6 +848,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
     if (const char* env = std::getenv("BNX_HEAVY_KMIN")) c->heavy_kmin = std::strtoull(env, nullptr, 10);
+    if (const char* env = std::getenv("BNX_HEAVY_GRID")) c->heavy_grid = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
         const int v = std::atoi(env);
         if (v >= 0 && v < screen_variant_count()) c->screen_v = v;
