@@ -245,6 +245,23 @@ def test_heavy_candidates_beyond_the_paper(orc):
         assert bp.last_stats()["candidates"] == exact_candidates(orc, lo, hi), (lo, hi)
 
 
+def test_heavy_boundaries(orc):
+    """Domains where the heavy generator switches arithmetic (neighbours below / above 2^32:
+    32-bit tests vs residues), single-integer domains and the very start: exact candidate
+    counts against the oracle and identical rows to the byte screen."""
+    cases = [(2**32 - 2**20, 2**32 + 2**20), (2**32 - 3, 2**32 + 3), (1, 1), (1, 2), (2, 2), (3, 8),
+             (1214, 1216), (2**33 + 7, 2**33 + 7)]
+    for lo, hi in cases:
+        rows = {}
+        for name in ("heavy", "screen"):
+            with engine(name):
+                rows[name] = np.ascontiguousarray(bp.search.search_rows(lo, hi)).tobytes()
+                cand = bp.last_stats()["candidates"]
+                if hi - lo < 2**22:
+                    assert cand == exact_candidates(orc, lo, hi), (name, lo, hi)
+        assert rows["heavy"] == rows["screen"], (lo, hi)
+
+
 @pytest.mark.parametrize("lo,hi", [(1, 2**32 - 1), (2**32, 2**33 - 1), (2**40 - 2**30, 2**40 - 1),
                                    (1_400_000_000_000 - 2**28, 1_400_000_000_000), (2**42 - 2**26, 2**42 - 2)])
 def test_engines_agree(lo, hi):
