@@ -163,6 +163,7 @@ struct bnx_ctx {
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
     uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
     int heavy_grid = 0;       // tuning only (BNX_HEAVY_GRID, CTAs per SM); 0 = default
+    uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
     DBuf<ulonglong2> q1;
     DBuf<BnxCand> cand;
@@ -579,6 +580,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.flags = c->flags.p;
     ha.shard = c->shard;
     ha.nshards = c->nshards;
+    ha.tail_heavy = c->tail_heavy ? c->tail_heavy : TAIL_HEAVY;
     // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
     // (8 resident CTAs per SM at 32 registers) below ~2^33; more, smaller runs when the sieve
     // shares the GPU
@@ -849,6 +851,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
     if (const char* env = std::getenv("BNX_HEAVY_KMIN")) c->heavy_kmin = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_HEAVY_GRID")) c->heavy_grid = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("BNX_TAIL_HEAVY")) c->tail_heavy = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
         const int v = std::atoi(env);
         if (v >= 0 && v < screen_variant_count()) c->screen_v = v;

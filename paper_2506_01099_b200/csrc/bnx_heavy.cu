@@ -482,7 +482,7 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
     atomicAdd(&a.ctr[CTR_CAND], 1ull);
     if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
     atomicMax(&a.ctr[CTR_MAXCHK], (unsigned long long)total);
-    if (total > TAIL_HEAVY) {
+    if (total > a.tail_heavy) {
         const unsigned long long h = atomicAdd(&a.ctr[CTR_HEAVY], 1ull);
         if (h < a.heavy_cap) a.heavy[h] = c;
     } else {

@@ -24,9 +24,9 @@ constexpr int SIEVE_MAXS = 160;
 // [8] heavy engine: candidates in the light list (k_tail); the rest went to the heavy queue
 constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_NEXT = 5, CTR_MAXCHK = 6,
               CTR_HEAVY = 7, CTR_LIGHT = 8, CTR_N = 9;
-// Candidates with more than this many residue-class members are handed to k_tail_heavy,
+// Candidates with more than this many residue-class members are handed to k_tail_heavy
 // which spreads their members over many warps (one candidate below 2^32 has ~1,500).
-constexpr uint64_t TAIL_HEAVY = 128;
+constexpr uint64_t TAIL_HEAVY = 48;
 
 struct ScreenArgs {
     uint64_t x_begin;  // multiple of the tile
@@ -104,6 +104,7 @@ struct HeavyArgs {
     unsigned long long* ctr;
     int* flags;             // [1] k outside kinfo (internal error)
     uint32_t shard, nshards;  // this search covers items/chunks [shard, shard + 1) / nshards
+    uint64_t tail_heavy;      // candidates with more residue-class members go to k_tail_heavy
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
 cudaError_t heavy_configure();
