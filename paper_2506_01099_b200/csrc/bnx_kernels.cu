@@ -439,11 +439,17 @@ __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
     const int lane = threadIdx.x & 31;
     const uint64_t cnt = a.cands ? min((uint64_t)a.ctr[CTR_LIGHT], a.cand_cap)
                                  : min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
+    // the first round is static (warp w takes item w: no contended atomic when the grid has a
+    // warp per item), later items come one at a time from a shared counter
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t first = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     for (;;) {
-        // survivors / candidates are taken one at a time from a shared counter
-        unsigned long long i = 0;
-        if (lane == 0) i = atomicAdd(&a.ctr[CTR_NEXT], 1ull);
-        i = __shfl_sync(0xffffffffu, i, 0);
+        unsigned long long i = first;
+        if (first == ~0ull) {
+            if (lane == 0) i = nwarps + atomicAdd(&a.ctr[CTR_NEXT], 1ull);
+            i = __shfl_sync(0xffffffffu, i, 0);
+        }
+        first = ~0ull;
         if (i >= cnt) break;
         uint64_t n, r0, r1;
         if (a.cands) {  // heavy engine: radicals known exactly, R <= 2n already checked
