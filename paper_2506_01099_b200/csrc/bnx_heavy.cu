@@ -109,8 +109,18 @@ __global__ void k_heavy_count(HeavyArgs a) {
             if (lo > kl) kl = lo;
         }
         const uint64_t c = kh >= kl ? kh - kl + 1 : 0;
-        a.cnt[i] = c >= a.kmin ? ((c + a.kc - 1) / a.kc) << 40 : c;  // sieve chunks | trial items
-        a.klo[i] = c ? (uint32_t)kl : 0u;
+        if (c >= a.kmin) {  // sieve chunks over every k
+            a.cnt[i] = ((c + a.kc - 1) / a.kc) << 40;
+            a.klo[i] = (uint32_t)kl;
+        } else if (e.rmask & 1u) {  // trial items; sigma even: only odd k can be canonical
+            const uint64_t ko = kl | 1u;
+            const uint64_t co = kh >= ko ? (kh - ko) / 2 + 1 : 0;
+            a.cnt[i] = co;
+            a.klo[i] = co ? (uint32_t)ko : 0u;
+        } else {
+            a.cnt[i] = c;
+            a.klo[i] = c ? (uint32_t)kl : 0u;
+        }
         a.kcnt[i] = (uint32_t)c;
     }
 }
@@ -259,7 +269,8 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
             if (w < b1) {
                 i = first_class_above(a.incl, cls0, a.nent, w);
                 const BnxHeavyEnt e = a.ent[i];
-                const uint64_t k = a.klo[i] + (w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0));
+                // item -> k: every k, or every odd k when sigma is even (see k_heavy_count)
+                const uint64_t k = a.klo[i] + ((w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0)) << (e.rmask & 1u));
                 if (k < a.nkinfo) {
                     bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
                     if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
