@@ -112,3 +112,31 @@ def test_engine_selection(L, ctx):
     assert rows[0] == rows[1] and len(rows[0]) == 25
     assert L.bnx_ctx_set_engine(ctx, 7) == 4
     assert L.bnx_ctx_engine(ctx) == 0
+
+
+def test_graph_replay_follows_parameter_changes():
+    """The heavy engine replays its search as CUDA graphs: changing the domain, the kinds,
+    the stream or the timing switch must re-capture (same rows as a fresh context), and a
+    repeat must replay with identical rows and counters."""
+    import torch
+
+    c = _native.Context(0)
+    try:
+        want = {}
+        fresh = _native.Context(0)
+        try:
+            for lo, hi, kinds in ((1, 2**24, 3), (5_000_000, 2**24, 1), (1, 2**24, 2)):
+                want[(lo, hi, kinds)] = fresh.search_domain(lo, hi, kinds, None, 0).tobytes()
+        finally:
+            fresh.close()
+        s = torch.cuda.Stream()
+        for timing in (False, True):
+            c.set_timing(timing)
+            for stream in (0, s.cuda_stream):
+                c.set_stream(stream)
+                for key, rows in want.items():
+                    for _ in range(2):
+                        assert c.search_domain(key[0], key[1], key[2], None, 0).tobytes() == rows
+        c.set_stream(0)
+    finally:
+        c.close()
