@@ -109,9 +109,14 @@ __global__ void k_heavy_count(HeavyArgs a) {
             if (lo > kl) kl = lo;
         }
         const uint64_t c = kh >= kl ? kh - kl + 1 : 0;
-        if (c >= a.kmin) {  // sieve chunks over every k
-            a.cnt[i] = ((c + a.kc - 1) / a.kc) << 40;
-            a.klo[i] = (uint32_t)kl;
+        if (c >= a.kmin) {  // sieve chunks over every k (every odd k when sigma is even)
+            const uint64_t st = (e.rmask & 1u) ? 2 : 1;
+            const uint64_t ks = st == 2 ? (kl | 1u) : kl;
+            const uint64_t cs = kh >= ks ? (kh - ks) / st + 1 : 0;
+            a.cnt[i] = ((cs + a.kc - 1) / a.kc) << 40;
+            a.klo[i] = (uint32_t)ks;
+            a.kcnt[i] = (uint32_t)cs;  // listed k (index space)
+            continue;
         } else if (e.rmask & 1u) {  // trial items; sigma even: only odd k can be canonical
             const uint64_t ko = kl | 1u;
             const uint64_t co = kh >= ko ? (kh - ko) / 2 + 1 : 0;
@@ -121,7 +126,7 @@ __global__ void k_heavy_count(HeavyArgs a) {
             a.cnt[i] = c;
             a.klo[i] = c ? (uint32_t)kl : 0u;
         }
-        a.kcnt[i] = (uint32_t)c;
+        a.kcnt[i] = 0;  // (sieve classes only)
     }
 }
 
@@ -331,7 +336,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
     uint32_t* s_task = s_kcm + np2;                                            // ntasks
     uint32_t* s_list = s_task + a.ntasks;                                      // kc
     __shared__ BnxHeavyEnt s_e;
-    __shared__ uint64_t s_k0, s_kend, s_cls_end, s_cls;
+    __shared__ uint64_t s_k0, s_kend, s_cls_end, s_cls, s_kfirst;
     __shared__ int s_nl, s_fresh;
     const int tid = threadIdx.x;
     for (int j = tid; j < np2; j += blockDim.x) {
@@ -370,8 +375,9 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                 if (tid == 0) {
                     const uint64_t first = cls ? a.incl[cls - 1] >> 40 : 0;
                     s_e = a.ent[cls];
-                    s_k0 = (uint64_t)a.klo[cls] + (ch - first) * (uint64_t)kc;
-                    s_kend = (uint64_t)a.klo[cls] + a.kcnt[cls];
+                    s_k0 = (ch - first) * (uint64_t)kc;  // index of the chunk's first listed k
+                    s_kend = a.kcnt[cls];                 // listed k of the class
+                    s_kfirst = a.klo[cls];
                     s_cls_end = a.incl[cls] >> 40;
                     s_cls = cls;
                     s_fresh = 1;
@@ -384,8 +390,9 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         }
         __syncthreads();
         const BnxHeavyEnt e = s_e;
-        const uint64_t k0 = s_k0;
-        const int kn = (int)min((uint64_t)kc, s_kend - k0);
+        const uint32_t st = (e.rmask & 1u) ? 2 : 1;  // listed k: every k, or every odd k
+        const int kn = (int)min((uint64_t)kc, s_kend - s_k0);
+        const uint64_t k0 = s_kfirst + st * s_k0;  // the k of index 0 of this chunk
         const bool fresh = s_fresh;
         // 1. progressions (full set-up on entering a class, else shifted by kc)
         for (int j = tid; j < np2; j += blockDim.x) {
@@ -398,8 +405,10 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                 } else {
                     const uint32_t inv = a.invtab[a.invoff[j] + bm];
                     const uint32_t k0m = (uint32_t)mod_by_lim(k0, p, lim);
-                    s_off[2 * j] = (int32_t)((2 * p - inv - k0m) % p);  // k = -b^-1: p | k b + 1
-                    s_off[2 * j + 1] = (int32_t)((inv + p - k0m) % p);  // k = +b^-1: p | k b - 1
+                    // index i of k0 + st i: (root - k0) st^-1 mod p (st^-1 = (p+1)/2 for st = 2)
+                    const uint32_t ist = st == 2 ? (p + 1) / 2 : 1;
+                    s_off[2 * j] = (int32_t)((2 * p - inv - k0m) % p * ist % p);  // k = -b^-1: p | k b + 1
+                    s_off[2 * j + 1] = (int32_t)((inv + p - k0m) % p * ist % p);  // k = +b^-1: p | k b - 1
                 }
             } else if (s_off[2 * j] >= 0) {
                 const uint32_t d = p - s_kcm[j];
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         }
         // 3. canonical k of the chunk
         for (int kk = tid; kk < kn; kk += blockDim.x) {
-            const uint64_t k = k0 + kk;
+            const uint64_t k = k0 + (uint64_t)st * kk;
             if (k >= a.nkinfo) { a.flags[1] = 1; continue; }
             bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
             if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         const uint64_t sigma = e.m * e.r;
         for (int li = tid; li < nl; li += blockDim.x) {
             const uint32_t kk = s_list[li];
-            const uint64_t k = k0 + kk;
+            const uint64_t k = k0 + (uint64_t)st * kk;
             const uint64_t x = k * e.b;
             const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
             const bool vU = x >= a.n_first && x <= a.n_last;
