@@ -542,8 +542,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.ntasks = h.ntasks;
     ha.kc = kc;
     // measured (scripts/engine_compare.py, KMIN sweep): with <= 64 primes below P2 (bounds
-    // up to ~2^33) trial division is as fast as the sieve; above, sieving classes with >= 512
-    // k is best (2^40: 5.8 ms vs 8.3 ms)
+    // up to ~2^33) trial division is as fast as the sieve; above, sieving classes with >= 256
+    // k is best (measured sweep at 2^40)
     ha.kmin = c->heavy_kmin ? c->heavy_kmin : (np2 <= 64 ? ~0ull : HEAVY_KMIN_DEFAULT);
     ha.invtab = h.invtab.p;
     ha.invoff = h.invoff.p;

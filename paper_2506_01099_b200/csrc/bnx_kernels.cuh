@@ -67,7 +67,7 @@ constexpr int HEAVY_NP3 = 7000;  // odd primes <= cbrt(y_max) staged in shared m
 // Classes with at least HEAVY_KMIN values of k in a domain are sieved over k (k_heavy_sieve)
 // in chunks of up to kc values; the rest go through trial division (k_heavy_screen).  Item
 // counts are packed: low 40 bits trial items, high 24 bits sieve chunks (one scan).
-constexpr uint64_t HEAVY_KMIN_DEFAULT = 512;
+constexpr uint64_t HEAVY_KMIN_DEFAULT = 256;
 constexpr uint64_t HEAVY_TRIAL_MASK = (1ull << 40) - 1;
 constexpr int HEAVY_TASK_HITS = 16;  // marks per sieve task (host-built task list)
 constexpr int HEAVY_HITS = 8;        // hit-list slots per (k, side) in k_heavy_sieve (more: trial division)
