@@ -150,8 +150,8 @@ struct HeavyItem {
     uint64_t x, sigma, radx;
 };
 
-// The y tests of one heavy x (both sides), see the file comment.  Shared tables: (inv, lim)
-// and p of the odd primes <= P2.
+// The y tests of one heavy x (both sides), see the file comment.  Shared tables per odd
+// prime <= P2: (p^-1 mod 2^64, floor((2^64-1)/p)), the same mod 2^32, p, and 2^32 mod p.
 __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
                                         const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32) {
     const uint64_t x = it.x;
@@ -305,7 +305,9 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
 
 // Classes with many k: y = k b -+ 1 runs through an arithmetic progression in k, so for an
 // odd prime p not dividing b, p | k b + 1 <=> k = -b^-1 and p | k b - 1 <=> k = +b^-1 (mod p).
-// Each CTA owns runs of chunks (up to kc consecutive k of one class each):
+// A class with sigma even lists only its odd k (index i -> k = k0 + 2i; the progression
+// offsets are multiplied by 2^-1 mod p).  Each CTA owns runs of chunks (up to kc listed k
+// of one class each):
 //   1. per prime <= P2, on entering a class: b mod p (Barrett with the table's
 //      floor((2^64-1)/p)), b^-1 mod p (host table), the first index of each side's
 //      progression in the chunk; for the next chunk of the same class the indices just
@@ -608,7 +610,7 @@ size_t heavy_sieve_smem(int np2, int kc, int ntasks) {
 }
 
 // Dynamic shared memory limits of the heavy kernels, set once per device (outside any
-// stream capture): the sieve's masks and the exact stage's prime table can exceed 48 KB.
+// stream capture): the sieve's hit lists and the exact stage's prime table exceed 48 KB.
 cudaError_t heavy_configure() {
     cudaError_t e = cudaFuncSetAttribute(k_heavy_sieve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e == cudaSuccess)
