@@ -114,7 +114,6 @@ struct HeavyTab {
     int ntasks = 0, tasks_np2 = -1, tasks_kc = 0;
     DBuf<unsigned char> scan_temp;
     size_t scan_bytes = 0;
-    std::vector<uint64_t> sigma;  // host mirror: sigma of each class, ascending
     void release() {
         ent.release();
         kinfo.release();
@@ -430,11 +429,9 @@ int build_heavy(bnx_ctx* c, uint64_t max_x) {
             }
         }
     }
-    // by sigma: a domain [x_lo, x_hi] only needs the classes with 2 sigma^2 >= x_lo (a suffix)
-    std::sort(ents.begin(), ents.end(),
-              [](const BnxHeavyEnt& u, const BnxHeavyEnt& v) { return u.m * u.r < v.m * v.r; });
-    h.sigma.resize(ents.size());
-    for (size_t i = 0; i < ents.size(); ++i) h.sigma[i] = ents[i].m * ents[i].r;
+    // (kept in DFS order: classes of one prime structure stay together, which measured ~10%
+    // faster at 2^32 than sorting by sigma, and the host sort cost 0.35 s at 2^40, 7 s at 2^48;
+    // classes with no k in a domain simply count zero items)
     const uint64_t K = isqrt_u64(max_x / 2) + 3;
     std::vector<uint32_t> kinfo(K, 0);
     for (size_t i = 0; i < 31 && i < P.size(); ++i)
@@ -547,11 +544,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.kmin = c->heavy_kmin ? c->heavy_kmin : (np2 <= 64 ? ~0ull : HEAVY_KMIN_DEFAULT);
     ha.invtab = h.invtab.p;
     ha.invoff = h.invoff.p;
-    // first class with 2 sigma^2 >= n_first (smaller sigma have no heavy x in the domain)
-    const uint64_t smin = isqrt_u64(n_first / 2);
-    const uint64_t start = (uint64_t)(std::lower_bound(h.sigma.begin(), h.sigma.end(), smin) - h.sigma.begin());
-    ha.ent = h.ent.p + start;
-    ha.nent = h.nent - start;
+    ha.ent = h.ent.p;
+    ha.nent = h.nent;
     ha.cnt = h.cnt.p;
     ha.incl = h.incl.p;
     ha.klo = h.klo.p;
