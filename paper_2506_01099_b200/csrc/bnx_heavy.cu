@@ -146,6 +146,25 @@ __device__ __forceinline__ uint64_t first_class_above(const uint64_t* __restrict
     return lo;
 }
 
+// The same search by a whole warp: 32 probes per round narrow [lo, hi] 32-fold, so a run's
+// first class costs ~4 dependent L2 loads instead of ~2 log2(nent) (requires w < incl[n-1]).
+// CHUNKS: search the sieve-chunk prefix (incl >> 40) instead of the trial-item prefix.
+template <bool CHUNKS = false>
+__device__ __forceinline__ uint64_t first_class_above_warp(const uint64_t* __restrict__ incl, uint64_t n,
+                                                           uint64_t w, int lane) {
+    uint64_t lo = 0, hi = n - 1;  // the answer lies in [lo, hi]
+    while (lo < hi) {
+        const uint64_t span = hi - lo;
+        const uint64_t v = incl[lo + span * (lane + 1) / 32];
+        const bool above = (CHUNKS ? v >> 40 : v & HEAVY_TRIAL_MASK) > w;
+        const int j = __ffs(__ballot_sync(0xFFFFFFFFu, above)) - 1;  // lane 31 probes hi: j >= 0
+        const uint64_t nlo = j ? lo + span * j / 32 + 1 : lo;
+        hi = lo + span * (j + 1) / 32;
+        lo = nlo;
+    }
+    return lo;
+}
+
 struct HeavyItem {
     uint64_t x, sigma, radx;
 };
@@ -167,58 +186,48 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
     // instead of a 64-bit multiply (the kernel is IMAD-pipe bound).
     const bool narrow = yU < (1ull << 32);
     const uint32_t x32 = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    // One bit per prime for both sides (an odd p divides at most one of x - 1, x + 1); the
+    // side is found in the post-pass.  The table is padded to a multiple of 32 (the padding
+    // bits are masked off) so that the loop unrolls with constant bit positions.
     for (int j0 = 0; j0 < a.np2; j0 += 32) {
         const int jn = min(32, a.np2 - j0);
-        uint32_t mL = 0, mU = 0;
+        uint32_t m = 0;
         if (narrow) {
             // one multiply per prime for both sides: (x -+ 1) p^-1 = x p^-1 -+ p^-1 (mod 2^32)
-#pragma unroll 8
-            for (int u = 0; u < jn; ++u) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
                 const uint2 d = s_pd32[j0 + u];
                 const uint32_t t = x32 * d.x;
-                mL |= (uint32_t)(t - d.x <= d.y) << u;
-                mU |= (uint32_t)(t + d.x <= d.y) << u;
+                m |= (uint32_t)(min(t - d.x, t + d.x) <= d.y) << u;
             }
-            mL = vL ? mL : 0u;
         } else {
             // x >= 2^32 (x < 2^53): w = x_lo + x_hi (2^32 mod p) is x mod p shifted into 32
             // bits (a carry out of the add is 2^32 = 2^32 mod p); then the same test on w -+ 1.
             // w - 1 and w + 1 can wrap at 0 and 2^32 - 1: such rare false bits are rejected by
             // the exact division check below.
-#pragma unroll 8
-            for (int u = 0; u < jn; ++u) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
                 const uint2 d = s_pd32[j0 + u];
                 const uint32_t cp = s_c32[j0 + u];
                 uint32_t w = x32 + xh * cp;
                 if (w < x32) w += cp;
                 const uint32_t t = w * d.x;
-                mL |= (uint32_t)(t - d.x <= d.y) << u;
-                mU |= (uint32_t)(t + d.x <= d.y) << u;
+                m |= (uint32_t)(min(t - d.x, t + d.x) <= d.y) << u;
             }
-            mL = vL ? mL : 0u;
         }
-        while (mL | mU) {  // one hit of each side per round: the rounds are shared
-            if (mL) {
-                const int u = __ffs(mL) - 1;
-                mL &= mL - 1;
-                const ulonglong2 d = s_il[j0 + u];
-                const uint64_t pp = s_p[j0 + u];
-                uint64_t t = cL * d.x;
-                if (t <= d.y) {  // p | cL exactly (rejects a wrapped false bit)
-                    cL = t;
-                    for (t = cL * d.x; t <= d.y; t = cL * d.x) { cL = t; sL *= pp; }
-                }
-            }
-            if (mU) {
-                const int u = __ffs(mU) - 1;
-                mU &= mU - 1;
-                const ulonglong2 d = s_il[j0 + u];
-                const uint64_t pp = s_p[j0 + u];
-                uint64_t t = cU * d.x;
-                if (t <= d.y) {
-                    cU = t;
-                    for (t = cU * d.x; t <= d.y; t = cU * d.x) { cU = t; sU *= pp; }
-                }
+        if (jn < 32) m &= (1u << jn) - 1;
+        while (m) {  // exact division of the side the prime divides (with its powers)
+            const int u = __ffs(m) - 1;
+            m &= m - 1;
+            const ulonglong2 d = s_il[j0 + u];
+            const uint64_t pp = s_p[j0 + u];
+            uint64_t t = cL * d.x;
+            if (vL && t <= d.y) {  // p | cL exactly (rejects a wrapped false bit)
+                cL = t;
+                for (t = cL * d.x; t <= d.y; t = cL * d.x) { cL = t; sL *= pp; }
+            } else if ((t = cU * d.x) <= d.y) {
+                cU = t;
+                for (t = cU * d.x; t <= d.y; t = cU * d.x) { cU = t; sU *= pp; }
             }
         }
     }
@@ -238,9 +247,11 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
 // takes one and runs the y tests, so the expensive part always runs with full warps.
 __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) {
     constexpr int T = HEAVY_THREADS;
-    extern __shared__ ulonglong2 s_il[];  // np2 (inv, lim), np2 (inv32, lim32), np2 p, np2 2^32 mod p
+    // np2 (inv, lim), np2p (inv32, lim32), np2 p, np2p 2^32 mod p (np2p: np2 padded to 32)
+    extern __shared__ ulonglong2 s_il[];
+    const int np2p = (a.np2 + 31) & ~31;
     uint2* s_pd32 = reinterpret_cast<uint2*>(s_il + a.np2);
-    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + a.np2);
+    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + np2p);
     uint32_t* s_c32 = s_p + a.np2;
     __shared__ HeavyItem s_q[2 * T];
     __shared__ int s_cnt;
@@ -252,6 +263,10 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         s_p[j] = (uint32_t)a.pdiv[j].p;
         s_c32[j] = (uint32_t)((1ull << 32) % a.pdiv[j].p);
     }
+    for (int j = a.np2 + tid; j < np2p; j += T) {  // padding (its bits are masked off)
+        s_pd32[j] = make_uint2(1u, 0u);
+        s_c32[j] = 0u;
+    }
     if (tid == 0) s_cnt = 0;
     if (a.nent == 0) return;
     // the trial items in gridDim * nshards equal runs; CTA g of shard s takes run g * nshards + s,
@@ -259,7 +274,10 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     const uint64_t Wt = a.incl[a.nent - 1] & HEAVY_TRIAL_MASK;
     const uint64_t nb = (uint64_t)gridDim.x * a.nshards, blk = (uint64_t)blockIdx.x * a.nshards + a.shard;
     const uint64_t b0 = Wt * blk / nb, b1 = Wt * (blk + 1) / nb;
-    if (tid == 0 && b0 < b1) s_cls = first_class_above(a.incl, 0, a.nent, b0);
+    if (tid < 32 && b0 < b1) {
+        const uint64_t c0 = first_class_above_warp(a.incl, a.nent, b0, tid);
+        if (tid == 0) s_cls = c0;
+    }
     __syncthreads();
     uint64_t base = b0;
     // `cnt` is every thread's copy of s_cnt, read only between the two barriers of a fill
@@ -357,13 +375,8 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
             const bool enter = ch == c_begin || ch >= s_cls_end;
             if (enter) {
                 uint64_t cls;
-                if (ch == c_begin) {  // first chunk of the run: binary search
-                    uint64_t lo = 0, hi = a.nent - 1;  // first class with chunk prefix > ch
-                    while (lo < hi) {
-                        const uint64_t mid = (lo + hi) >> 1;
-                        if ((a.incl[mid] >> 40) > ch) hi = mid; else lo = mid + 1;
-                    }
-                    cls = lo;
+                if (ch == c_begin) {  // first chunk of the run: first class with chunk prefix > ch
+                    cls = first_class_above_warp<true>(a.incl, a.nent, ch, tid);
                 } else {  // the next sieve class: the 32 lanes probe the following classes
                     uint64_t from = s_cls + 1;
                     for (;;) {
@@ -641,7 +654,9 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
             k_heavy_sieve<<<grid, 256, smemS, aux>>>(a);
             cudaEventRecord(ev_join, aux);
         }
-        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint2) + 2 * sizeof(uint32_t));
+        const size_t np2p = (size_t)(a.np2 + 31) & ~(size_t)31;  // (see k_heavy_screen)
+        const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint32_t)) +
+                             np2p * (sizeof(uint2) + sizeof(uint32_t));
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
     }
