@@ -162,6 +162,8 @@ struct bnx_ctx {
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
     uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
     int heavy_grid = 0;       // tuning only (BNX_HEAVY_GRID, CTAs per SM); 0 = default
+    int heavy_runs = -1;      // tuning only (BNX_HEAVY_RUNS, fetched screen runs per CTA); -1 = default
+    int heavy_run_first = -1; // tuning only (BNX_HEAVY_RUN_FIRST, static share /256); -1 = default
     uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
     DBuf<ulonglong2> q1;
@@ -580,6 +582,11 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // shares the GPU
     const int grid_mult = c->heavy_grid ? c->heavy_grid : (ha.kmin == ~0ull ? 8 : 20);
     const int grid = c->num_sms * grid_mult;
+    // measured (scripts/sweep_env.sh BNX_HEAVY_RUNS / BNX_HEAVY_RUN_FIRST): in the one-wave
+    // case, half the items in static runs and the rest in 2 fetched runs per CTA (-10% at
+    // 2^32); with several waves (sieve bounds) the CTA scheduler already balances
+    ha.run_mult = c->heavy_runs >= 0 ? (uint32_t)c->heavy_runs : (ha.kmin == ~0ull ? 2u : 0u);
+    ha.run_first = c->heavy_run_first >= 0 ? (uint32_t)c->heavy_run_first : 128u;
     TailArgs ta;
     std::memset(&ta, 0, sizeof(ta));
     ta.cands = c->cand.p;
@@ -845,6 +852,8 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
     if (const char* env = std::getenv("BNX_HEAVY_KMIN")) c->heavy_kmin = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_HEAVY_GRID")) c->heavy_grid = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("BNX_HEAVY_RUNS")) c->heavy_runs = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("BNX_HEAVY_RUN_FIRST")) c->heavy_run_first = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_TAIL_HEAVY")) c->tail_heavy = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
         const int v = std::atoi(env);

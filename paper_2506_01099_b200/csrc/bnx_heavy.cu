@@ -269,23 +269,49 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     }
     if (tid == 0) s_cnt = 0;
     if (a.nent == 0) return;
-    // the trial items in gridDim * nshards equal runs; CTA g of shard s takes run g * nshards + s,
-    // so every shard samples the whole class range (the classes differ in canonical density)
+    // The trial items in gridDim * run_mult * nshards equal runs; run r of shard s is run
+    // r * nshards + s, so every shard samples the whole class range (the classes differ in
+    // canonical density).  CTA g starts with run g and then fetches runs from a counter, so
+    // CTAs that drew sparse runs take more of them (the SMs finish together).
     const uint64_t Wt = a.incl[a.nent - 1] & HEAVY_TRIAL_MASK;
-    const uint64_t nb = (uint64_t)gridDim.x * a.nshards, blk = (uint64_t)blockIdx.x * a.nshards + a.shard;
-    const uint64_t b0 = Wt * blk / nb, b1 = Wt * (blk + 1) / nb;
-    if (tid < 32 && b0 < b1) {
-        const uint64_t c0 = first_class_above_warp(a.incl, a.nent, b0, tid);
-        if (tid == 0) s_cls = c0;
-    }
-    __syncthreads();
-    uint64_t base = b0;
+    const uint64_t WA = a.run_mult ? Wt * min(a.run_first, 256u) / 256 : Wt;  // items of the static runs
+    const uint64_t nr = (uint64_t)gridDim.x * (1 + a.run_mult);
+    __shared__ unsigned long long s_run;
+    uint64_t run = blockIdx.x, b1 = 0, base = 0;
+    bool more = true;
     // `cnt` is every thread's copy of s_cnt, read only between the two barriers of a fill
     // step (after all appends, before the next) so that the loop conditions agree.
     int cnt = 0;
     for (;;) {
-        // fill the queue up to at least T entries (or until the run is exhausted)
-        while (cnt < T && base < b1) {
+        // fill the queue up to at least T entries (or until the runs are exhausted)
+        while (cnt < T && more) {
+            if (base >= b1) {  // next run
+                if (run == ~0ull) {
+                    if (tid == 0) s_run = gridDim.x + atomicAdd(&a.ctr[CTR_RUNS], 1ull);
+                    __syncthreads();
+                    run = s_run;
+                }
+                if (run >= nr) {
+                    more = false;
+                    break;
+                }
+                if (run < gridDim.x) {  // static run
+                    const uint64_t blk = run * a.nshards + a.shard, nb = (uint64_t)gridDim.x * a.nshards;
+                    base = WA * blk / nb;
+                    b1 = WA * (blk + 1) / nb;
+                } else {
+                    const uint64_t blk = (run - gridDim.x) * a.nshards + a.shard, nb = (nr - gridDim.x) * a.nshards;
+                    base = WA + (Wt - WA) * blk / nb;
+                    b1 = WA + (Wt - WA) * (blk + 1) / nb;
+                }
+                run = ~0ull;
+                if (tid < 32 && base < b1) {
+                    const uint64_t c0 = first_class_above_warp(a.incl, a.nent, base, tid);
+                    if (tid == 0) s_cls = c0;
+                }
+                __syncthreads();
+                continue;
+            }
             const uint64_t w = base + tid;
             const uint64_t cls0 = s_cls;
             uint64_t i = cls0;

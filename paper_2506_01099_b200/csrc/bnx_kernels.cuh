@@ -23,7 +23,7 @@ constexpr int SIEVE_MAXS = 160;
 // [7] heavy candidates queued for k_tail_heavy
 // [8] heavy engine: candidates in the light list (k_tail); the rest went to the heavy queue
 constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_NEXT = 5, CTR_MAXCHK = 6,
-              CTR_HEAVY = 7, CTR_LIGHT = 8, CTR_N = 9;
+              CTR_HEAVY = 7, CTR_LIGHT = 8, CTR_RUNS = 9, CTR_N = 10;
 // Candidates with more than this many residue-class members are handed to k_tail_heavy
 // which spreads their members over many warps (one candidate below 2^32 has ~1,500).
 constexpr uint64_t TAIL_HEAVY = 48;
@@ -105,6 +105,8 @@ struct HeavyArgs {
     int* flags;             // [1] k outside kinfo (internal error)
     uint32_t shard, nshards;  // this search covers items/chunks [shard, shard + 1) / nshards
     uint64_t tail_heavy;      // candidates with more residue-class members go to k_tail_heavy
+    uint32_t run_mult;        // k_heavy_screen: fetched runs per CTA (from CTR_RUNS) after the first
+    uint32_t run_first;       // k_heavy_screen: share of the items in the first (static) runs, /256
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
 cudaError_t heavy_configure();
