@@ -27,6 +27,7 @@
 // canonical heavy x below 2^32 (instead of 2^32 integers), each costing ~54 trial divisions
 // per side.  Every kernel here can run one shard of a search (HeavyArgs::shard, multi-GPU).
 #include <cub/device/device_scan.cuh>
+#include <type_traits>
 
 #include "bnx_kernels.cuh"
 #include "bnx_rad.cuh"
@@ -77,6 +78,28 @@ __device__ __forceinline__ uint64_t surplus_bound(uint64_t c, const HeavyArgs& a
         if (!a.cube_filter || m63 == 1 || m63 == 8 || m63 == 55 || m63 == 62) {
             const uint64_t r = (uint64_t)rintf(cbrtf(cf));
             if (r * r * r == c && r * r > u) u = r * r;
+        }
+    }
+    return u;
+}
+
+// The same for c < 2^32 in 32-bit arithmetic (narrow y: the 64-bit remainder and products
+// are most of the bound's cost).
+__device__ __forceinline__ uint64_t surplus_bound32(uint32_t c, const HeavyArgs& a) {
+    if (c < a.p1sq) return 1;
+    uint32_t u = 1;
+    const float cf = (float)c;
+    if ((c & 7) == 1) {
+        const uint32_t q = (uint32_t)rintf(sqrtf(cf));  // q < 2^16 (q = 2^16 wraps to 0 != c)
+        if (q * q == c) u = q;
+    }
+    if (c >= a.p1cube) {
+        const uint32_t v = (uint32_t)(sqrtf(cf * a.inv_p1f) * 1.0001f) + 1;
+        if (v > u) u = v;
+        const uint32_t m63 = c % 63u;
+        if (!a.cube_filter || m63 == 1 || m63 == 8 || m63 == 55 || m63 == 62) {
+            const uint64_t r = (uint64_t)rintf(cbrtf(cf));
+            if (r * r * r == c && r * r > u) u = (uint32_t)(r * r);
         }
     }
     return u;
@@ -171,28 +194,29 @@ struct HeavyItem {
 
 // The y tests of one heavy x (both sides), see the file comment.  Shared tables per odd
 // prime <= P2: (p^-1 mod 2^64, floor((2^64-1)/p)), the same mod 2^32, p, and 2^32 mod p.
-__device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
-                                        const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32) {
+// NARROW: both y below 2^32 -- every test, division and bound in 32-bit arithmetic (the
+// kernel is bound by its ALU/IMAD instruction count).
+template <bool NARROW>
+__device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
+                                             const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32) {
+    using W = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     const uint64_t x = it.x;
     const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
     const bool vU = x >= a.n_first && x <= a.n_last;
     const uint64_t yL = vL ? x - 1 : 1, yU = x + 1;
     const int tL = __ffsll((long long)yL) - 1, tU = __ffsll((long long)yU) - 1;
-    uint64_t cL = yL >> tL, cU = yU >> tU;
-    uint64_t sL = tL ? 1ull << (tL - 1) : 1ull, sU = tU ? 1ull << (tU - 1) : 1ull;
-    // Divisibility of the odd parts by 32 primes at a time into bit masks (branch-free: the
-    // lanes of a warp stay converged), then the hits (about 1.5 per y) are divided out fully.
-    // Both y below 2^32 (domains below 2^32): 32-bit tests, one IMAD per prime and side
-    // instead of a 64-bit multiply (the kernel is IMAD-pipe bound).
-    const bool narrow = yU < (1ull << 32);
+    W cL = (W)(yL >> tL), cU = (W)(yU >> tU);
+    W sL = tL ? (W)1 << (tL - 1) : (W)1, sU = tU ? (W)1 << (tU - 1) : (W)1;
     const uint32_t x32 = (uint32_t)x, xh = (uint32_t)(x >> 32);
-    // One bit per prime for both sides (an odd p divides at most one of x - 1, x + 1); the
-    // side is found in the post-pass.  The table is padded to a multiple of 32 (the padding
-    // bits are masked off) so that the loop unrolls with constant bit positions.
+    // Divisibility by 32 primes at a time into a bit mask, branch-free (the lanes of a warp
+    // stay converged): one bit per prime for both sides (an odd p divides at most one of
+    // x - 1, x + 1), the side is found in the post-pass.  The table is padded to a multiple
+    // of 32 (the padding bits are masked off) so that the loop unrolls with constant bit
+    // positions.  Then the hits (about 1.5 per y) are divided out with their powers.
     for (int j0 = 0; j0 < a.np2; j0 += 32) {
         const int jn = min(32, a.np2 - j0);
         uint32_t m = 0;
-        if (narrow) {
+        if constexpr (NARROW) {
             // one multiply per prime for both sides: (x -+ 1) p^-1 = x p^-1 -+ p^-1 (mod 2^32)
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
@@ -219,26 +243,51 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
         while (m) {  // exact division of the side the prime divides (with its powers)
             const int u = __ffs(m) - 1;
             m &= m - 1;
-            const ulonglong2 d = s_il[j0 + u];
-            const uint64_t pp = s_p[j0 + u];
-            uint64_t t = cL * d.x;
-            if (vL && t <= d.y) {  // p | cL exactly (rejects a wrapped false bit)
+            W inv, lim;
+            if constexpr (NARROW) {
+                const uint2 d = s_pd32[j0 + u];
+                inv = d.x;
+                lim = d.y;
+            } else {
+                const ulonglong2 d = s_il[j0 + u];
+                inv = d.x;
+                lim = d.y;
+            }
+            const W pp = s_p[j0 + u];
+            W t = cL * inv;
+            if (vL && t <= lim) {  // p | cL exactly (rejects a wrapped false bit)
                 cL = t;
-                for (t = cL * d.x; t <= d.y; t = cL * d.x) { cL = t; sL *= pp; }
-            } else if ((t = cU * d.x) <= d.y) {
+                for (t = cL * inv; t <= lim; t = cL * inv) { cL = t; sL *= pp; }
+            } else if ((t = cU * inv) <= lim) {
                 cU = t;
-                for (t = cU * d.x; t <= d.y; t = cU * d.x) { cU = t; sU *= pp; }
+                for (t = cU * inv; t <= lim; t = cU * inv) { cU = t; sU *= pp; }
             }
         }
     }
-    const bool pL = vL && twice_prod_ge(it.sigma, sL * surplus_bound(cL, a), x);
-    const bool pU = vU && twice_prod_ge(it.sigma, sU * surplus_bound(cU, a), x + 1);
+    uint64_t uL, uU;
+    if constexpr (NARROW) {
+        uL = surplus_bound32(cL, a);
+        uU = surplus_bound32(cU, a);
+    } else {
+        uL = surplus_bound(cL, a);
+        uU = surplus_bound(cU, a);
+    }
+    const bool pL = vL && twice_prod_ge(it.sigma, (uint64_t)sL * uL, x);
+    const bool pU = vU && twice_prod_ge(it.sigma, (uint64_t)sU * uU, x + 1);
     if (pL || pU) {
         const unsigned long long slot = atomicAdd(&a.ctr[CTR_SURV], (unsigned long long)(pL + pU));
         if (pL && slot < a.q1_cap) a.q1[slot] = make_ulonglong2((x - 1) | (1ull << 63), it.radx);
         const unsigned long long s2 = slot + pL;
         if (pU && s2 < a.q1_cap) a.q1[s2] = make_ulonglong2(x, it.radx);
     }
+}
+
+__device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
+                                        const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32) {
+    if (it.x + 1 < (1ull << 32))
+        y_tests_impl<true>(a, it, s_il, s_p, s_pd32, s_c32);
+    else
+        y_tests_impl<false>(a, it, s_il, s_p, s_pd32, s_c32);
 }
 
 // Each CTA owns a contiguous run of items and walks it in windows of HEAVY_THREADS (thread t
