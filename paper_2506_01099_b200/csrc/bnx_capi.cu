@@ -84,6 +84,7 @@ struct Tables {
     uint64_t gen = ~0ull;
     DBuf<BnxProg> small, large;
     DBuf<BnxPDiv> pdiv;
+    DBuf<uint4> pd32;  // the first primes of pdiv: (p^-1 mod 2^32, floor((2^32-1)/p), p, 2^32 mod p)
     DBuf<uint32_t> items;
     int nitems = 0;
     uint32_t nsmall = 0;
@@ -92,6 +93,7 @@ struct Tables {
         small.release();
         large.release();
         pdiv.release();
+        pd32.release();
         items.release();
         gen = ~0ull;
     }
@@ -381,6 +383,12 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
     if (!items.empty())
         CK(cudaMemcpyAsync(t.items.p, items.data(), sizeof(uint32_t) * items.size(), cudaMemcpyHostToDevice,
                            c->stream));
+    {  // 32-bit divisibility constants of the heavy path's trial primes (<= cbrt(S))
+        const uint64_t n32 = std::min<uint64_t>(npd, HEAVY_NP3);
+        TRY(t.pd32.ensure(n32 + 1));
+        launch_pdiv32(t.pdiv.p, n32, t.pd32.p, c->stream);
+        CK(cudaGetLastError());
+    }
     CK(cudaStreamSynchronize(c->stream));  // the host vectors above must outlive the copies
     t.nitems = (int)items.size();
     t.nsmall = ns;
@@ -558,6 +566,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.n_first = n_first;
     ha.n_last = n_last;
     ha.pdiv = t.pdiv.p;
+    ha.pd32 = t.pd32.p;
     ha.np2 = (int)np2;
     ha.np3 = np3;
     ha.p1 = p2 + 1;

@@ -308,9 +308,10 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     const int tid = threadIdx.x;
     for (int j = tid; j < a.np2; j += T) {
         s_il[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
-        s_pd32[j] = make_uint2((uint32_t)a.pdiv[j].inv, 0xFFFFFFFFu / (uint32_t)a.pdiv[j].p);  // p^-1 mod 2^32
-        s_p[j] = (uint32_t)a.pdiv[j].p;
-        s_c32[j] = (uint32_t)((1ull << 32) % a.pdiv[j].p);
+        const uint4 q = a.pd32[j];
+        s_pd32[j] = make_uint2(q.x, q.y);
+        s_p[j] = q.z;
+        s_c32[j] = q.w;
     }
     for (int j = a.np2 + tid; j < np2p; j += T) {  // padding (its bits are masked off)
         s_pd32[j] = make_uint2(1u, 0u);
@@ -612,9 +613,10 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
     const int np3 = (int)a.np3;
     for (int j = threadIdx.x; j < np3; j += blockDim.x) {
         s_il3[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
-        s_pd3[j] = make_uint2((uint32_t)a.pdiv[j].inv, 0xFFFFFFFFu / (uint32_t)a.pdiv[j].p);
-        s_p3[j] = (uint32_t)a.pdiv[j].p;
-        s_c3[j] = (uint32_t)((1ull << 32) % a.pdiv[j].p);
+        const uint4 q = a.pd32[j];
+        s_pd3[j] = make_uint2(q.x, q.y);
+        s_p3[j] = q.z;
+        s_c3[j] = q.w;
     }
     __syncthreads();
     const uint64_t nq = min((uint64_t)a.ctr[CTR_SURV], a.q1_cap);
@@ -691,6 +693,13 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
 
 }  // namespace
 
+__global__ void k_pdiv32(const BnxPDiv* __restrict__ pdiv, uint64_t n, uint4* __restrict__ out) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = (uint32_t)pdiv[j].p;
+        out[j] = make_uint4((uint32_t)pdiv[j].inv, 0xFFFFFFFFu / p, p, (uint32_t)((1ull << 32) % p));
+    }
+}
+
 size_t heavy_sieve_smem(int np2, int kc, int ntasks) {
     return sizeof(uint16_t) * (size_t)2 * kc * HEAVY_HITS + (size_t)2 * kc +
            (sizeof(ulonglong2) + 2 * sizeof(uint32_t) + 2 * sizeof(int32_t)) * np2 +
@@ -706,6 +715,10 @@ cudaError_t heavy_configure() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_heavy_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     return e;
+}
+
+void launch_pdiv32(const BnxPDiv* pdiv, uint64_t n, uint4* out, cudaStream_t st) {
+    if (n) k_pdiv32<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 1024), 256, 0, st>>>(pdiv, n, out);
 }
 
 size_t heavy_scan_temp_bytes(uint64_t nent) {

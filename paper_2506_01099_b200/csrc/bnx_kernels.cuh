@@ -89,6 +89,7 @@ struct HeavyArgs {
     uint64_t x_lo, x_hi;    // heavy x range: [n_first, n_last + 1]
     uint64_t n_first, n_last;
     const BnxPDiv* pdiv;    // odd primes ascending
+    const uint4* pd32;      // the same primes (<= cbrt(y_max)): (p^-1 mod 2^32, floor((2^32-1)/p), p, 2^32 mod p)
     int np2;                // odd primes <= P2 = floor(y_max^(1/4))
     uint64_t np3;           // odd primes <= cbrt(y_max)
     uint64_t p1, p1sq, p1cube;  // P2 + 1 and its powers
@@ -109,6 +110,7 @@ struct HeavyArgs {
     uint32_t run_first;       // k_heavy_screen: share of the items in the first (static) runs, /256
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
+void launch_pdiv32(const BnxPDiv* pdiv, uint64_t n, uint4* out, cudaStream_t st);
 cudaError_t heavy_configure();
 size_t heavy_sieve_smem(int np2, int kc, int ntasks);
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
