@@ -46,14 +46,26 @@ BNX_D uint64_t bnx_gcd64(uint64_t a, uint64_t b) {
     return a << sh;
 }
 
-// u | r^inf, i.e. every prime of u divides r (rad(u) | r).  u >= 1, r >= 1.
+// u | r^inf, i.e. every prime of u divides r (rad(u) | r).  1 <= u < 2^63, r >= 1.
+// Branch-free (the lanes of a warp stay converged): the twos first, then for the odd part
+// u | r^64 (every odd prime exponent of u is below 64) by six Montgomery squarings mod u.
+// Montgomery products carry a factor 2^-64, a unit mod odd u, so the result is 0 exactly
+// when r^64 is; no conversion into or out of the Montgomery domain is needed.
+BNX_D uint64_t bnx_redc(uint64_t hi, uint64_t lo, uint64_t u, uint64_t nu) {  // (hi:lo) 2^-64 mod u
+    const uint64_t m = lo * nu;                                                 // nu = -u^-1 mod 2^64
+    uint64_t t = hi + __umul64hi(m, u) + (lo != 0);                             // < 2u (hi:lo < u 2^64)
+    return t >= u ? t - u : t;
+}
+
 BNX_D bool bnx_supported_by(uint64_t u, uint64_t r) {
-    while (u > 1) {
-        uint64_t g = bnx_gcd64(u, r);
-        if (g == 1) return false;
-        u /= g;
-    }
-    return true;
+    const int tz = __ffsll((long long)u) - 1;
+    const bool twos_ok = tz == 0 || (r & 1) == 0;
+    u >>= tz;
+    const uint64_t nu = 0 - bnx_inv64(u);
+    uint64_t x = bnx_redc(0, r, u, nu);  // r 2^-64 mod u (r < 2^64 <= u 2^64)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) x = bnx_redc(__umul64hi(x, x), x * x, u, nu);
+    return twos_ok && (u == 1 || x == 0);
 }
 
 // floor(4 * log2(v)) for v >= 1, exact: 4e + #{k in 1..3 : mantissa >= 2^(k/4)}.
