@@ -383,15 +383,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_screen(ScreenArgs a) {
 //       second kind: rad(n), rad(n+1) both divide n + m + 1  ->  m = tR - n - 1
 //     so the lanes walk those t; m is kept iff rad(m), rad(m+1) equal the required
 //     radicals, tested exactly: rad(m) == r  <=>  r | m  and  m / r | r^inf (gcds).
-//  3. every kept m is verified by full radical comparison (rad_warp of m and m+1) and
-//     classified as the reference does (signatures.py:67-81), then emitted.
+//  3. every kept m is classified as the reference does (signatures.py:67-81) and emitted:
+//     the two tests fix rad(m) and rad(m+1) exactly, so no radical is recomputed.
 // One candidate n (R = r0 r1 <= 2n) and a range [k_begin, k_end) of its residue-class members:
 // k < t1 -> first kind m = n - (k+1) R; else second kind m = (t0 + k - t1) R - n - 1.  With
 // s0 = n / r0 and s1 = (n+1) / r1 the cofactors are linear in t, so no division is needed:
 //   first kind   m / r0 = s0 - t r1,   (m+1) / r1 = s1 - t r0
 //   second kind  m / r1 = t r0 - s1,   (m+1) / r0 = t r1 - s0
-// and m is kept iff both cofactors are supported by their radical (u | r^inf).  Kept m are
-// verified by full radical comparison and classified (signatures.py:67-81).  Warp-collective.
+// and m is kept iff both cofactors are supported by their radical (u | r^inf), which makes
+// rad(m) and rad(m+1) the required radicals exactly (signatures.py:67-81 classifies).
+// Warp-collective.
 struct TailCand {
     uint64_t n, r0, r1, R, s0, s1, t0, t1;
 };
@@ -413,22 +414,15 @@ __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_be
                 ok = bnx_supported_by(t * c.r0 - c.s1, c.r1) && bnx_supported_by(t * c.r1 - c.s0, c.r0);
             }
         }
-        uint32_t bal = __ballot_sync(0xffffffffu, ok);
-        while (bal) {
-            const int src = __ffs(bal) - 1;
-            bal &= bal - 1;
-            const uint64_t mm = __shfl_sync(0xffffffffu, m, src);
-            uint64_t rm, rm1;
-            rad2_warp(mm, a.pdiv, a.npdiv, rm, rm1);
-            int kind = 0;
-            if (rm == c.r0 && rm1 == c.r1) kind = 1;
-            else if (rm == c.r1 && rm1 == c.r0) kind = 2;
-            if (lane == 0) {
-                atomicAdd(&a.ctr[CTR_MATCH], 1ull);
-                if (kind && (a.kinds & (1u << (kind - 1))) && mm >= 1 && mm < c.n) {
-                    unsigned long long s = atomicAdd(&a.ctr[CTR_PAIRS], 1ull);
-                    if (s < a.pair_cap) a.pairs[s] = bnx_pair_t{mm, c.n, rm, rm1, kind, 0};
-                }
+        // A kept m has its radicals exactly: r0 | m (m = n - tR) and m / r0 | r0^inf give
+        // rad(m) = r0 (r0 squarefree), and likewise for m + 1 and for the second kind.
+        if (ok) {
+            const int kind = k < c.t1 ? 1 : 2;
+            atomicAdd(&a.ctr[CTR_MATCH], 1ull);
+            if ((a.kinds & (1u << (kind - 1))) && m >= 1 && m < c.n) {
+                const unsigned long long s = atomicAdd(&a.ctr[CTR_PAIRS], 1ull);
+                if (s < a.pair_cap)
+                    a.pairs[s] = kind == 1 ? bnx_pair_t{m, c.n, c.r0, c.r1, 1, 0} : bnx_pair_t{m, c.n, c.r1, c.r0, 2, 0};
             }
         }
     }
