@@ -605,18 +605,77 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
 // Exact radical of the other side (one thread per survivor: the odd primes <= cbrt(y_max)
 // from shared memory, 32 per bit mask as in y_tests; the cofactor is then 1, p, p^2 or pq),
 // the exact test R <= 2n, de-duplication, emission.
+// rad(o) of an odd o < 2^53 by one thread: trial division by the odd primes <= cbrt(y_max)
+// (32 at a time into a bit mask, unrolled with constant bit positions over the table padded
+// to a multiple of 32), then at most two primes remain (p, p^2 or pq).  NARROW: o < 2^32,
+// everything in 32-bit arithmetic.
+template <bool NARROW>
+__device__ __forceinline__ uint64_t rad_odd_thread(uint64_t o, int np3, const ulonglong2* s_il3, const uint2* s_pd3,
+                                                   const uint32_t* s_p3, const uint32_t* s_c3) {
+    using W = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
+    W c = (W)o, rad = 1;
+    const uint32_t ol = (uint32_t)o, oh = (uint32_t)(o >> 32);
+    for (int j0 = 0; j0 < np3; j0 += 32) {
+        const int jn = min(32, np3 - j0);
+        uint32_t m = 0;
+        if constexpr (NARROW) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const uint2 d = s_pd3[j0 + u];
+                m |= (uint32_t)(ol * d.x <= d.y) << u;
+            }
+        } else {  // o = oh 2^32 + ol: w = ol + oh (2^32 mod p) = o (mod p) in 32 bits (p, oh < 2^16)
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const uint2 d = s_pd3[j0 + u];
+                const uint32_t cp = s_c3[j0 + u];
+                uint32_t w = ol + oh * cp;
+                if (w < ol) w += cp;
+                m |= (uint32_t)(w * d.x <= d.y) << u;
+            }
+        }
+        if (jn < 32) m &= (1u << jn) - 1;
+        while (m) {
+            const int u = __ffs(m) - 1;
+            m &= m - 1;
+            W inv, lim;
+            if constexpr (NARROW) {
+                inv = s_pd3[j0 + u].x;
+                lim = s_pd3[j0 + u].y;
+            } else {
+                inv = s_il3[j0 + u].x;
+                lim = s_il3[j0 + u].y;
+            }
+            rad *= (W)s_p3[j0 + u];
+            c *= inv;
+            while (c * inv <= lim) c *= inv;
+        }
+    }
+    uint64_t r = rad;
+    if (c > 1) {  // at most two primes > cbrt(y) remain: c = p, p^2 or pq
+        const uint64_t q = exact_sqrt(c);
+        r *= q ? q : (uint64_t)c;
+    }
+    return r;
+}
+
 __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
-    extern __shared__ ulonglong2 s_il3[];  // np3 (inv, lim), np3 (inv32, lim32), np3 p, np3 2^32 mod p
-    uint2* s_pd3 = reinterpret_cast<uint2*>(s_il3 + a.np3);
-    uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_pd3 + a.np3);
-    uint32_t* s_c3 = s_p3 + a.np3;
-    const int np3 = (int)a.np3;
+    // np3 (inv, lim), np3p (inv32, lim32), np3 p, np3p 2^32 mod p (np3p: np3 padded to 32)
+    extern __shared__ ulonglong2 s_il3[];
+    const int np3 = (int)a.np3, np3p = (np3 + 31) & ~31;
+    uint2* s_pd3 = reinterpret_cast<uint2*>(s_il3 + np3);
+    uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_pd3 + np3p);
+    uint32_t* s_c3 = s_p3 + np3;
     for (int j = threadIdx.x; j < np3; j += blockDim.x) {
         s_il3[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
         const uint4 q = a.pd32[j];
         s_pd3[j] = make_uint2(q.x, q.y);
         s_p3[j] = q.z;
         s_c3[j] = q.w;
+    }
+    for (int j = np3 + threadIdx.x; j < np3p; j += blockDim.x) {  // padding (its bits are masked off)
+        s_pd3[j] = make_uint2(1u, 0u);
+        s_c3[j] = 0u;
     }
     __syncthreads();
     const uint64_t nq = min((uint64_t)a.ctr[CTR_SURV], a.q1_cap);
@@ -647,41 +706,8 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         const uint64_t y = sideL ? n : n + 1;
         const int tz = __ffsll((long long)y) - 1;
         const uint64_t o = y >> tz;
-        uint64_t c = o, rady = tz ? 2 : 1;
-        const bool narrow = o < (1ull << 32);  // 32-bit tests (see y_tests)
-        const uint32_t ol = (uint32_t)o, oh = (uint32_t)(o >> 32);
-        for (int j0 = 0; j0 < np3; j0 += 32) {
-            const int jn = min(32, np3 - j0);
-            uint32_t m = 0;
-            if (narrow) {
-#pragma unroll 8
-                for (int u = 0; u < jn; ++u) {
-                    const uint2 d = s_pd3[j0 + u];
-                    m |= (uint32_t)((uint32_t)o * d.x <= d.y) << u;
-                }
-            } else {  // o = oh 2^32 + ol: w = ol + oh (2^32 mod p) = o (mod p) in 32 bits (p, oh < 2^16)
-#pragma unroll 8
-                for (int u = 0; u < jn; ++u) {
-                    const uint2 d = s_pd3[j0 + u];
-                    const uint32_t cp = s_c3[j0 + u];
-                    uint32_t w = ol + oh * cp;
-                    if (w < ol) w += cp;
-                    m |= (uint32_t)(w * d.x <= d.y) << u;
-                }
-            }
-            while (m) {
-                const int u = __ffs(m) - 1;
-                m &= m - 1;
-                const ulonglong2 d = s_il3[j0 + u];
-                rady *= s_p3[j0 + u];
-                c *= d.x;
-                while (c * d.x <= d.y) c *= d.x;
-            }
-        }
-        if (c > 1) {  // at most two primes > cbrt(y) remain: c = p, p^2 or pq
-            const uint64_t q = exact_sqrt(c);
-            rady *= q ? q : c;
-        }
+        const uint64_t rady = (tz ? 2 : 1) * (o < (1ull << 32) ? rad_odd_thread<true>(o, np3, s_il3, s_pd3, s_p3, s_c3)
+                                                               : rad_odd_thread<false>(o, np3, s_il3, s_pd3, s_p3, s_c3));
         if (__umul64hi(radx, rady) != 0 || radx * rady > 2 * n) continue;
         if (sideL) {  // keep from x = n + 1 only if n itself is not heavy
             const uint64_t sy = y / rady;
@@ -748,7 +774,8 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
     }
-    const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint2) + 2 * sizeof(uint32_t));
+    const size_t np3p = (size_t)(a.np3 + 31) & ~(size_t)31;  // (see k_heavy_exact)
+    const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t)) + np3p * (sizeof(uint2) + sizeof(uint32_t));
     k_heavy_exact<<<grid, 256, smem3, st>>>(a);
     if (ev_generated) cudaEventRecord(ev_generated, st);
 }
