@@ -173,11 +173,19 @@ struct bnx_ctx {
 
     DBuf<uint64_t> surv;
     DBuf<BnxCand> heavy;
-    DBuf<bnx_pair_t> pairs;
-    DBuf<unsigned long long> ctr;
-    DBuf<int> flags;
-    unsigned long long* h_ctr = nullptr;
-    int* h_flags = nullptr;
+    DBuf<int> flags;  // (radical sieve)
+    int* h_flags = nullptr;  // (radical sieve)
+    // The search's device I/O block: counters, flags and the pair rows in one allocation, so
+    // one copy reads back the counters, flags and the first PAIR_PREFIX rows (h_io, pinned).
+    DBuf<unsigned char> io;
+    unsigned long long* ctr_p = nullptr;
+    int* sflags_p = nullptr;
+    bnx_pair_t* pairs_p = nullptr;
+    size_t pairs_cap = 0;
+    unsigned char* h_io = nullptr;
+    unsigned long long* h_sctr = nullptr;
+    int* h_sflags = nullptr;
+    bnx_pair_t* h_pairs = nullptr;
 
     DBuf<uint32_t> t_nsmall;
     DBuf<unsigned long long> t_nlarge;
@@ -469,14 +477,36 @@ int build_heavy(bnx_ctx* c, uint64_t max_x) {
     return BNX_OK;
 }
 
+// (Re)allocate the I/O block for `rows` pair rows (the counters are reset by every search).
+int ensure_pairs(bnx_ctx* c, size_t rows) {
+    rows = std::max<size_t>(rows, PAIR_PREFIX);
+    TRY(c->io.ensure(IO_PAIRS + sizeof(bnx_pair_t) * rows));
+    c->ctr_p = reinterpret_cast<unsigned long long*>(c->io.p + IO_CTR);
+    c->sflags_p = reinterpret_cast<int*>(c->io.p + IO_FLAGS);
+    c->pairs_p = reinterpret_cast<bnx_pair_t*>(c->io.p + IO_PAIRS);
+    c->pairs_cap = (c->io.cap - IO_PAIRS) / sizeof(bnx_pair_t);
+    return BNX_OK;
+}
+
 int ensure_work(bnx_ctx* c) {
     if (!c->surv.p) TRY(c->surv.ensure(1 << 20));
     if (!c->heavy.p) TRY(c->heavy.ensure(64));
-    if (!c->pairs.p) TRY(c->pairs.ensure(1 << 14));
-    TRY(c->ctr.ensure(CTR_N));
-    TRY(c->flags.ensure(4));
-    if (!c->h_ctr) CK(cudaMallocHost(&c->h_ctr, sizeof(unsigned long long) * CTR_N));
-    if (!c->h_flags) CK(cudaMallocHost(&c->h_flags, sizeof(int) * 4));
+    if (!c->pairs_p) TRY(ensure_pairs(c, 1 << 14));
+    if (!c->h_io) {
+        CK(cudaMallocHost(&c->h_io, IO_PAIRS + sizeof(bnx_pair_t) * PAIR_PREFIX));
+        c->h_sctr = reinterpret_cast<unsigned long long*>(c->h_io + IO_CTR);
+        c->h_sflags = reinterpret_cast<int*>(c->h_io + IO_FLAGS);
+        c->h_pairs = reinterpret_cast<bnx_pair_t*>(c->h_io + IO_PAIRS);
+    }
+    return BNX_OK;
+}
+
+// The read-back at the end of every search, one copy: counters, flags and the first
+// PAIR_PREFIX pair rows (every search up to 2^48 has fewer: 49 of both kinds), so collect()
+// needs no second copy.
+int read_back(bnx_ctx* c) {
+    CK(cudaMemcpyAsync(c->h_io, c->io.p, IO_PAIRS + sizeof(bnx_pair_t) * PAIR_PREFIX, cudaMemcpyDeviceToHost,
+                       c->stream));
     return BNX_OK;
 }
 
@@ -581,8 +611,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.heavy = c->heavy.p;
     ha.heavy_cap = c->heavy.cap;
     ha.kinds = kinds;
-    ha.ctr = c->ctr.p;
-    ha.flags = c->flags.p;
+    ha.ctr = c->ctr_p;
+    ha.flags = c->sflags_p;
     ha.shard = c->shard;
     ha.nshards = c->nshards;
     ha.tail_heavy = c->tail_heavy ? c->tail_heavy : TAIL_HEAVY;
@@ -605,13 +635,13 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ta.pdiv = t.pdiv.p;
     ta.npdiv = t.npdiv;
     ta.kinds = kinds;
-    ta.pairs = c->pairs.p;
-    ta.pair_cap = c->pairs.cap;
-    ta.ctr = c->ctr.p;
+    ta.pairs = c->pairs_p;
+    ta.pair_cap = c->pairs_cap;
+    ta.ctr = c->ctr_p;
     // two phases (generator; tail + read-back), so the timing events sit between them
     auto record_gen = [&]() -> int {
-        CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
-        CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+        CK(cudaMemsetAsync(c->ctr_p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+        CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
         launch_heavy(ha, h.scan_temp.p, h.scan_bytes, grid, c->stream, nullptr, c->aux, c->fork_ev, c->join_ev);
         CK(cudaGetLastError());
         return BNX_OK;
@@ -625,9 +655,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         launch_tail_light(ta, grid_for(c), c->stream);
         CK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
-        return BNX_OK;
+        return read_back(c);
     };
     if (!c->use_graphs) {
         if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
@@ -705,21 +733,20 @@ int enqueue_screen(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds
     const ScreenVariant& sv = screen_variant(c->screen_v);
     const uint64_t x_begin = n_first / sv.tile * sv.tile;
     const uint64_t ntiles = (n_last - x_begin) / sv.tile + 1;
-    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
-    CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+    CK(cudaMemsetAsync(c->ctr_p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+    CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
     ScreenArgs sa{x_begin, ntiles, n_first, n_last, t.small.p, (int)t.nsmall, t.large.p, (int)t.nlarge,
-                  t.items.p, t.nitems, c->surv.p, c->surv.cap, c->ctr.p, c->flags.p, c->screen_skip};
+                  t.items.p, t.nitems, c->surv.p, c->surv.cap, c->ctr_p, c->sflags_p, c->screen_skip};
     const int sgrid = (int)std::min<uint64_t>(ntiles, (uint64_t)c->num_sms * c->screen_blocks_per_sm);
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     sv.launch(sa, sgrid, c->stream);
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
-    TailArgs ta{c->surv.p, c->surv.cap, nullptr, 0, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs.p, c->pairs.cap,
-                c->ctr.p};
+    TailArgs ta{c->surv.p, c->surv.cap, nullptr, 0, c->heavy.p, c->heavy.cap, t.pdiv.p, t.npdiv, kinds, c->pairs_p, c->pairs_cap,
+                c->ctr_p};
     launch_tail(ta, grid_for(c), c->stream);
     CK(cudaGetLastError());
     if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
-    CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    TRY(read_back(c));
     c->q_valid = true;
     c->q_first = n_first;
     c->q_last = n_last;
@@ -733,10 +760,9 @@ int enqueue_screen(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds
 // A search with nothing to do (an empty shard): zeroed counters, no launches.
 int empty_search(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
     TRY(ensure_work(c));
-    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
-    CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
-    CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemsetAsync(c->ctr_p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+    CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
+    TRY(read_back(c));
     if (c->timing) {
         CK(cudaEventRecord(c->ev[0], c->stream));
         CK(cudaEventRecord(c->ev[1], c->stream));
@@ -771,24 +797,26 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
     if (!c->q_valid) return fail(BNX_ERR_INVALID, "no search enqueued");
     for (int attempt = 0; attempt < 8; ++attempt) {
         CK(cudaStreamSynchronize(c->stream));
-        if (c->h_flags[0]) return fail(BNX_ERR_CUDA, "screen bucket overflow");
-        const unsigned long long* h = c->h_ctr;
+        if (c->h_sflags[0]) return fail(BNX_ERR_CUDA, "screen bucket overflow");
+        const unsigned long long* h = c->h_sctr;
         bool again = false;
-        if (c->h_flags[1]) return fail(BNX_ERR_CUDA, "heavy generator: k outside its table");
+        if (c->h_sflags[1]) return fail(BNX_ERR_CUDA, "heavy generator: k outside its table");
         if (c->engine == 0) {
             if (h[CTR_SURV] > c->q1.cap) { TRY(c->q1.ensure(h[CTR_SURV] * 2)); again = true; }
             if (h[CTR_LIGHT] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_LIGHT] * 2)); again = true; }
         } else if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
         if (h[CTR_HEAVY] > c->heavy.cap) { TRY(c->heavy.ensure(h[CTR_HEAVY] * 2)); again = true; }
-        if (h[CTR_PAIRS] > c->pairs.cap) { TRY(c->pairs.ensure(h[CTR_PAIRS] * 2)); again = true; }
+        if (h[CTR_PAIRS] > c->pairs_cap) { TRY(ensure_pairs(c, h[CTR_PAIRS] * 2)); again = true; }
         if (again) {
             TRY(enqueue(c, c->q_first, c->q_last, c->q_kinds));
             continue;
         }
         const uint64_t np = h[CTR_PAIRS];
         rows.resize(np);
-        if (np) {
-            CK(cudaMemcpyAsync(rows.data(), c->pairs.p, sizeof(bnx_pair_t) * np, cudaMemcpyDeviceToHost, c->stream));
+        if (np <= PAIR_PREFIX) {
+            if (np) std::memcpy(rows.data(), c->h_pairs, sizeof(bnx_pair_t) * np);
+        } else {
+            CK(cudaMemcpyAsync(rows.data(), c->pairs_p, sizeof(bnx_pair_t) * np, cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
         }
         c->stats.survivors = h[CTR_SURV];
@@ -896,8 +924,7 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->cand.release();
     c->surv.release();
     c->heavy.release();
-    c->pairs.release();
-    c->ctr.release();
+    c->io.release();
     c->flags.release();
     c->t_nsmall.release();
     c->t_nlarge.release();
@@ -906,8 +933,8 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->sieve_out.release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
-    if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->h_flags) cudaFreeHost(c->h_flags);
+    if (c->h_io) cudaFreeHost(c->h_io);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->graph_exec2) cudaGraphExecDestroy(c->graph_exec2);

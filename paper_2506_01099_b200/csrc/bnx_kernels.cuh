@@ -22,8 +22,11 @@ constexpr int SIEVE_MAXS = 160;
 // [5] the tail's work queue head [6] most residue-class members of one candidate
 // [7] heavy candidates queued for k_tail_heavy
 // [8] heavy engine: candidates in the light list (k_tail); the rest went to the heavy queue
+constexpr size_t IO_CTR = 0, IO_FLAGS = 8 * 16, IO_PAIRS = 8 * 16 + 4 * 4 + 16;  // search I/O block (bnx_capi.cu)
+constexpr uint64_t PAIR_PREFIX = 64;   // pair rows read back with the counters (bnx_capi.cu read_back)
 constexpr int CTR_SURV = 0, CTR_CAND = 1, CTR_CHECKS = 2, CTR_MATCH = 3, CTR_PAIRS = 4, CTR_NEXT = 5, CTR_MAXCHK = 6,
               CTR_HEAVY = 7, CTR_LIGHT = 8, CTR_RUNS = 9, CTR_N = 10;
+static_assert(8 * CTR_N <= IO_FLAGS, "counters overlap the flags in the search I/O block");
 // Candidates with more than this many residue-class members are handed to k_tail_heavy
 // which spreads their members over many warps (one candidate below 2^32 has ~1,500).
 constexpr uint64_t TAIL_HEAVY = 48;
