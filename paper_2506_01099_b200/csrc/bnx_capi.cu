@@ -278,15 +278,17 @@ int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
     size_t k = (size_t)(std::upper_bound(primes, primes + np, need) - primes);
     TRY(c->stage64.ensure(k));
     TRY(c->primes.ensure(k));
-    if (k) {
-        CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->stream));
-        launch_narrow(c->stage64.p, k, c->primes.p, c->stream);
-        CK(cudaGetLastError());
-    }
-    // Tables derived from the primes are rebuilt only if the list actually changed (the copy
-    // above always happens: the caller's buffer is the input of every call).
+    // The copy always happens (the caller's buffer is the input of every call); the 32-bit
+    // device list and the tables derived from it are rebuilt only if the list changed.
     bool same = c->gen > 0 && c->h_primes.size() == k && c->primes_limit == need;
     for (size_t i = 0; same && i < k; ++i) same = c->h_primes[i] == (uint32_t)primes[i];
+    if (k) {
+        CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->stream));
+        if (!same) {
+            launch_narrow(c->stage64.p, k, c->primes.p, c->stream);
+            CK(cudaGetLastError());
+        }
+    }
     if (!same) {
         c->h_primes.resize(k);
         for (size_t i = 0; i < k; ++i) c->h_primes[i] = (uint32_t)primes[i];
