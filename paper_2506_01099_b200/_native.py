@@ -182,6 +182,8 @@ class Context:
         self.handle = handle
         self.device = device
         self.lock = threading.RLock()
+        self._buf = None
+        self._found = None
 
     def close(self) -> None:
         if self.handle:
@@ -259,17 +261,19 @@ class Context:
 
     # -- search ---------------------------------------------------------------------
     def _rows(self, fn) -> np.ndarray:
-        cap = 256
-        while True:
-            buf = (PairRow * cap)()
-            found = ctypes.c_size_t(0)
-            with self.lock:
-                st = check(fn(buf, cap, ctypes.byref(found)))
-            if st == BNX_BUFFER_FULL:
-                cap = int(found.value)
-                continue
-            arr = np.frombuffer(buf, dtype=PAIR_DTYPE, count=int(found.value)).copy()
-            return arr
+        # one row buffer per context, grown on BNX_BUFFER_FULL (the result is copied out)
+        with self.lock:
+            while True:
+                buf = self._buf
+                if buf is None:
+                    buf = self._buf = (PairRow * 256)()
+                    self._found = ctypes.c_size_t(0)
+                cap = len(buf)
+                st = check(fn(buf, cap, ctypes.byref(self._found)))
+                if st == BNX_BUFFER_FULL:
+                    self._buf = (PairRow * int(self._found.value))()
+                    continue
+                return np.frombuffer(buf, dtype=PAIR_DTYPE, count=int(self._found.value)).copy()
 
     def search(self, limit: int, kinds: int, primes: np.ndarray | None, primes_limit: int) -> np.ndarray:
         keep, pp, np_ = _prime_args(primes)  # noqa: F841 (keeps the array alive)

@@ -155,6 +155,7 @@ struct bnx_ctx {
     // prime table (device u32 + host mirror)
     DBuf<uint32_t> primes;
     std::vector<uint32_t> h_primes;
+    std::vector<uint64_t> h_primes64;  // the last caller-supplied list (memcmp: unchanged?)
     uint64_t primes_limit = 0;  // PrimeList.limit the table covers
     uint64_t gen = 0;           // bumps whenever the table changes
     DBuf<uint64_t> stage64;
@@ -260,6 +261,7 @@ int gen_primes(bnx_ctx* c, uint64_t limit) {
         offs.release();
     }
     c->h_primes.resize(total);
+    c->h_primes64.clear();
     CK(cudaMemcpyAsync(c->h_primes.data(), c->primes.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     base.release();
@@ -280,8 +282,8 @@ int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
     TRY(c->primes.ensure(k));
     // The copy always happens (the caller's buffer is the input of every call); the 32-bit
     // device list and the tables derived from it are rebuilt only if the list changed.
-    bool same = c->gen > 0 && c->h_primes.size() == k && c->primes_limit == need;
-    for (size_t i = 0; same && i < k; ++i) same = c->h_primes[i] == (uint32_t)primes[i];
+    const bool same = c->gen > 0 && c->h_primes64.size() == k && c->primes_limit == need &&
+                      (k == 0 || std::memcmp(c->h_primes64.data(), primes, sizeof(uint64_t) * k) == 0);
     if (k) {
         CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->stream));
         if (!same) {
@@ -292,6 +294,7 @@ int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
     if (!same) {
         c->h_primes.resize(k);
         for (size_t i = 0; i < k; ++i) c->h_primes[i] = (uint32_t)primes[i];
+        c->h_primes64.assign(primes, primes + k);
         c->primes_limit = need;  // the device copy holds exactly the primes <= need
         c->gen++;
     }
