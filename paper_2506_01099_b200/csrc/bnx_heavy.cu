@@ -318,6 +318,9 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         s_c32[j] = 0u;
     }
     if (tid == 0) s_cnt = 0;
+    // k_heavy_exact may be scheduled now (programmatic dependent launch): its CTAs take the
+    // SMs our CTAs leave and stage their prime tables before they wait for our completion
+    asm volatile("griddepcontrol.launch_dependents;");
     if (a.nent == 0) return;
     // The trial items in gridDim * run_mult * nshards equal runs; run r of shard s is run
     // r * nshards + s, so every shard samples the whole class range (the classes differ in
@@ -678,6 +681,9 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         s_c3[j] = 0u;
     }
     __syncthreads();
+    // launched as a programmatic dependent of k_heavy_screen: the tables above overlap its
+    // last CTAs; the survivors are read only after it has completed (and flushed)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t nq = min((uint64_t)a.ctr[CTR_SURV], a.q1_cap);
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
     if (nq * 32 <= nthreads) {
@@ -755,6 +761,7 @@ size_t heavy_scan_temp_bytes(uint64_t nent) {
 
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
                   cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+    bool pdl = false;
     if (a.nent) {
         const unsigned cb = (unsigned)std::min<uint64_t>((a.nent + 255) / 256, 4096);
         k_heavy_count<<<cb, 256, 0, st>>>(a);
@@ -773,10 +780,23 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
                              np2p * (sizeof(uint2) + sizeof(uint32_t));
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
+        pdl = !sieve;
     }
     const size_t np3p = (size_t)(a.np3 + 31) & ~(size_t)31;  // (see k_heavy_exact)
     const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t)) + np3p * (sizeof(uint2) + sizeof(uint32_t));
-    k_heavy_exact<<<grid, 256, smem3, st>>>(a);
+    {  // a programmatic dependent launch right after k_heavy_screen (see k_heavy_exact)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem3;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl ? 1 : 0;
+        cudaLaunchKernelEx(&cfg, k_heavy_exact, a);
+    }
     if (ev_generated) cudaEventRecord(ev_generated, st);
 }
 
