@@ -651,13 +651,16 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         CK(cudaGetLastError());
         return BNX_OK;
     };
+    // without timing events the whole search is one graph, and k_tail a programmatic
+    // dependent of k_heavy_exact
+    const bool single = c->use_graphs && !c->timing;
     auto record_tail = [&]() -> int {
         // k_tail_heavy (the few candidates with many residue-class members) overlaps k_tail
         CK(cudaEventRecord(c->fork_ev, c->stream));
         CK(cudaStreamWaitEvent(c->aux, c->fork_ev, 0));
         launch_tail_heavy(ta, c->aux);
         CK(cudaEventRecord(c->join_ev, c->aux));
-        launch_tail_light(ta, grid_for(c), c->stream);
+        launch_tail_light(ta, grid_for(c), c->stream, single);
         CK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
         CK(cudaGetLastError());
         return read_back(c);
@@ -671,14 +674,14 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     } else {
         // two graph launches replay the whole search (about ten stream operations): the host
         // enqueue cost and the inter-kernel gaps go; re-captured when any parameter changes
-        std::vector<unsigned char> key(sizeof(ha) + sizeof(ta) + 3 * sizeof(uint64_t));
+        std::vector<unsigned char> key(sizeof(ha) + sizeof(ta) + 4 * sizeof(uint64_t));
         unsigned char* kp = key.data();
         std::memcpy(kp, &ha, sizeof(ha));
         std::memcpy(kp + sizeof(ha), &ta, sizeof(ta));
-        const uint64_t extra[3] = {(uint64_t)(uintptr_t)c->stream, (uint64_t)grid,
-                                   (uint64_t)(uintptr_t)h.scan_temp.p ^ (uint64_t)h.scan_bytes << 1};
+        const uint64_t extra[4] = {(uint64_t)(uintptr_t)c->stream, (uint64_t)grid,
+                                   (uint64_t)(uintptr_t)h.scan_temp.p ^ (uint64_t)h.scan_bytes << 1, (uint64_t)single};
         std::memcpy(kp + sizeof(ha) + sizeof(ta), extra, sizeof(extra));
-        if (!c->graph_exec || !c->graph_exec2 || key != c->graph_key) {
+        if (!c->graph_exec || (!single && !c->graph_exec2) || key != c->graph_key) {
             for (auto* ge : {&c->graph_exec, &c->graph_exec2})
                 if (*ge) cudaGraphExecDestroy(*ge), *ge = nullptr;
             for (auto* g : {&c->graph, &c->graph2})
@@ -693,15 +696,23 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
                 CK(cudaGraphInstantiate(ge, *g, 0));
                 return BNX_OK;
             };
-            TRY(capture(record_gen, &c->graph, &c->graph_exec));
-            TRY(capture(record_tail, &c->graph2, &c->graph_exec2));
+            if (single) {
+                TRY(capture([&]() -> int { TRY(record_gen()); return record_tail(); }, &c->graph, &c->graph_exec));
+            } else {
+                TRY(capture(record_gen, &c->graph, &c->graph_exec));
+                TRY(capture(record_tail, &c->graph2, &c->graph_exec2));
+            }
             c->graph_key = key;
         }
-        if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
-        CK(cudaGraphLaunch(c->graph_exec, c->stream));
-        if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
-        CK(cudaGraphLaunch(c->graph_exec2, c->stream));
-        if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+        if (single) {
+            CK(cudaGraphLaunch(c->graph_exec, c->stream));
+        } else {
+            CK(cudaEventRecord(c->ev[0], c->stream));
+            CK(cudaGraphLaunch(c->graph_exec, c->stream));
+            CK(cudaEventRecord(c->ev[1], c->stream));
+            CK(cudaGraphLaunch(c->graph_exec2, c->stream));
+            CK(cudaEventRecord(c->ev[2], c->stream));
+        }
     }
     c->q_valid = true;
     c->q_first = n_first;

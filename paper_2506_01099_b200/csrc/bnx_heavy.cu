@@ -682,8 +682,10 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
     }
     __syncthreads();
     // launched as a programmatic dependent of k_heavy_screen: the tables above overlap its
-    // last CTAs; the survivors are read only after it has completed (and flushed)
+    // last CTAs; the survivors are read only after it has completed (and flushed).  k_tail
+    // (one-graph searches) may in turn be scheduled from here.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t nq = min((uint64_t)a.ctr[CTR_SURV], a.q1_cap);
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
     if (nq * 32 <= nthreads) {

@@ -430,6 +430,9 @@ __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_be
 
 
 __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
+    // (a programmatic dependent launch: wait for the producer grid's completion and flush;
+    // a no-op for an ordinary launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lane = threadIdx.x & 31;
     const uint64_t cnt = a.cands ? min((uint64_t)a.ctr[CTR_LIGHT], a.cand_cap)
                                  : min((uint64_t)a.ctr[CTR_SURV], a.surv_cap);
@@ -799,7 +802,18 @@ void launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
     k_tail<<<grid, 256, 0, st>>>(a);
     k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);
 }
-void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st) { k_tail<<<grid, 256, 0, st>>>(a); }
+void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;  // a programmatic dependent of k_heavy_exact (see k_tail)
+    cudaLaunchKernelEx(&cfg, k_tail, a);
+}
 void launch_tail_heavy(const TailArgs& a, cudaStream_t st) {
     k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);
 }

@@ -167,7 +167,7 @@ size_t sieve_smem_bytes();
 const void* sieve_kernel();
 void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st);
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st);
-void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st);  // heavy engine: k_tail only
+void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st, bool pdl = false);  // heavy engine: k_tail only
 void launch_tail_heavy(const TailArgs& a, cudaStream_t st);            // heavy engine: k_tail_heavy only
 void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st);
 void launch_prime_seg(uint64_t lo, uint64_t hi, const uint32_t* base, uint32_t nbase, uint32_t* counts,
