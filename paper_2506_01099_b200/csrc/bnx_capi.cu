@@ -645,8 +645,10 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ta.ctr = c->ctr_p;
     // two phases (generator; tail + read-back), so the timing events sit between them
     auto record_gen = [&]() -> int {
-        CK(cudaMemsetAsync(c->ctr_p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
-        CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
+        if (!ha.nent) {  // (otherwise k_heavy_count zeroes the counters and flags)
+            CK(cudaMemsetAsync(c->ctr_p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
+            CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
+        }
         launch_heavy(ha, h.scan_temp.p, h.scan_bytes, grid, c->stream, nullptr, c->aux, c->fork_ev, c->join_ev);
         CK(cudaGetLastError());
         return BNX_OK;

@@ -112,6 +112,10 @@ __device__ __forceinline__ bool twice_prod_ge(uint64_t sigma, uint64_t v, uint64
 }
 
 __global__ void k_heavy_count(HeavyArgs a) {
+    // the search's counters and flags start here (no memset launches; every later kernel
+    // runs after this one)
+    if (blockIdx.x == 0 && threadIdx.x < CTR_N) a.ctr[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 4) a.flags[threadIdx.x] = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.nent;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const BnxHeavyEnt e = a.ent[i];
