@@ -539,7 +539,14 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
                                         c->h_primes.begin());
         return (all && c->h_primes[0] == 2) ? all - 1 : all;
     };
-    const uint64_t np2 = std::min<uint64_t>(odd_upto(p2), t.npdiv), np3 = std::min<uint64_t>(odd_upto(p3), t.npdiv);
+    const uint64_t np3 = std::min<uint64_t>(odd_upto(p3), t.npdiv);
+    // stage-1 primes: the odd primes <= y_max^(1/4), rounded up to a multiple of 32 (the
+    // screen tests 32 per unrolled block anyway, and every extra prime tightens U(c): the
+    // bound only needs every prime factor of the cofactor to exceed the last prime tested)
+    const uint64_t np2 = std::min<uint64_t>({(odd_upto(p2) + 31) & ~31ull, t.npdiv, (uint64_t)HEAVY_NP3});
+    const uint64_t off2 = c->h_primes[0] == 2 ? 1 : 0;
+    const uint64_t p_last = np2 ? c->h_primes[np2 - 1 + off2] : 2;
+    const uint64_t p1 = np2 < t.npdiv ? c->h_primes[np2 + off2] : p_last + 1;  // smallest untested prime
     if (np2 > (uint64_t)HEAVY_NP2 || np3 > (uint64_t)HEAVY_NP3)
         return fail(BNX_ERR_RANGE, "bound too large for the heavy generator");
     // k_heavy_sieve: chunk length (masks of 32 primes per word, ~32 KB of shared memory) and
@@ -604,11 +611,11 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.pd32 = t.pd32.p;
     ha.np2 = (int)np2;
     ha.np3 = np3;
-    ha.p1 = p2 + 1;
+    ha.p1 = p1;
     ha.p1sq = ha.p1 * ha.p1;
     ha.p1cube = ha.p1sq * ha.p1;
     ha.inv_p1f = 1.0f / (float)ha.p1;
-    ha.cube_filter = p2 >= 7;
+    ha.cube_filter = p_last >= 7;
     ha.q1 = c->q1.p;
     ha.q1_cap = c->q1.cap;
     ha.cand = c->cand.p;
