@@ -15,6 +15,6 @@ done
 ncu --set full --import-source on --clock-control none -k k_heavy_sieve -s 1 -c 1 -o $O/full_2p40_k_heavy_sieve -f \
     python scripts/profile_search.py 40 3 > $O/ncu_sieve.log 2>&1
 python scripts/paper_range.py > $O/paper_range.jsonl 2> $O/paper_range.err
-python scripts/beyond_paper.py 2^44 2^45 2^46 2^47 2^48 > $O/beyond_paper.jsonl 2> $O/beyond.err
+python scripts/beyond_paper.py 1400000000000 2^44 2^45 2^46 2^47 2^48 > $O/beyond_paper.jsonl 2> $O/beyond.err
 { python scripts/shard_balance.py 2^40 8; python scripts/shard_balance.py 2^44 8; } > $O/shard_balance.jsonl 2> $O/shard.err
 ls -la $O
