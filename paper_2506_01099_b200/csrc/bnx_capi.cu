@@ -167,6 +167,7 @@ struct bnx_ctx {
     int heavy_grid = 0;       // tuning only (BNX_HEAVY_GRID, CTAs per SM); 0 = default
     int heavy_runs = -1;      // tuning only (BNX_HEAVY_RUNS, fetched screen runs per CTA); -1 = default
     int heavy_run_first = -1; // tuning only (BNX_HEAVY_RUN_FIRST, static share /256); -1 = default
+    int heavy_kc = 0;         // tuning only (BNX_HEAVY_KC, k per sieve chunk, multiple of 4); 0 = default
     uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
     DBuf<ulonglong2> q1;
@@ -553,7 +554,9 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // the marking tasks: prime j, side, sub-progression r of R, about HEAVY_TASK_HITS hits each
     const int W = (int)((np2 + 31) / 32);
     (void)W;
-    const int kc = 1536;  // hit lists: 2 x kc x (8 slots x 2 B + 1 B) = 51 KB of shared memory
+    // hit lists: 2 x kc x (8 slots x 2 B + 1 B) = 26 KB of shared memory at kc = 768 (measured
+    // sweep, BNX_HEAVY_KC: 768 beats 1536 by 7% at 2^40 and 14% at 2^48 -- twice the CTAs per SM)
+    const int kc = c->heavy_kc ? c->heavy_kc : 768;
     if (h.tasks_np2 != (int)np2 || h.tasks_kc != kc) {
         std::vector<uint32_t> tk, ioff;
         std::vector<uint16_t> itab;
@@ -630,8 +633,9 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.tail_heavy = c->tail_heavy ? c->tail_heavy : TAIL_HEAVY;
     // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
     // (8 resident CTAs per SM at 32 registers) below ~2^33; more, smaller runs when the sieve
-    // shares the GPU
-    const int grid_mult = c->heavy_grid ? c->heavy_grid : (ha.kmin == ~0ull ? 8 : 20);
+    // shares the GPU (40 per SM for domains of 2^38 or more: -2% at 2^40 and 2^44)
+    const int grid_mult = c->heavy_grid ? c->heavy_grid
+                                        : (ha.kmin == ~0ull ? 8 : (n_last - n_first >= (1ull << 38) ? 40 : 20));
     const int grid = c->num_sms * grid_mult;
     // measured (scripts/sweep_env.sh BNX_HEAVY_RUNS / BNX_HEAVY_RUN_FIRST): in the one-wave
     // case, half the items in static runs and the rest in 2 fetched runs per CTA (-10% at
@@ -916,6 +920,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_HEAVY_GRID")) c->heavy_grid = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_RUNS")) c->heavy_runs = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_RUN_FIRST")) c->heavy_run_first = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("BNX_HEAVY_KC")) c->heavy_kc = std::max(0, std::atoi(env)) & ~3;
     if (const char* env = std::getenv("BNX_TAIL_HEAVY")) c->tail_heavy = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
         const int v = std::atoi(env);
