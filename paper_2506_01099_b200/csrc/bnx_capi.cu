@@ -141,6 +141,8 @@ struct bnx_ctx {
     bool own_stream = false;
     cudaStream_t aux = nullptr;  // second stream: k_tail_heavy beside k_tail (heavy engine)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaEvent_t h2d_ev = nullptr;   // an unchanged prime list's copy, on `aux` beside the search
+    bool overlap_h2d = false, h2d_pending = false;
     // the heavy engine's search as a CUDA graph, re-captured whenever its parameters change
     bool use_graphs = true;
     cudaGraph_t graph = nullptr, graph2 = nullptr;
@@ -285,7 +287,13 @@ int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
     // device list and the tables derived from it are rebuilt only if the list changed.
     const bool same = c->gen > 0 && c->h_primes64.size() == k && c->primes_limit == need &&
                       (k == 0 || std::memcmp(c->h_primes64.data(), primes, sizeof(uint64_t) * k) == 0);
-    if (k) {
+    if (k && same && c->overlap_h2d) {
+        // nothing on the device reads this copy (the tables it would feed are current): it
+        // runs on the second stream beside the search and is joined before the call returns
+        CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->aux));
+        CK(cudaEventRecord(c->h2d_ev, c->aux));
+        c->h2d_pending = true;
+    } else if (k) {
         CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->stream));
         if (!same) {
             launch_narrow(c->stage64.p, k, c->primes.p, c->stream);
@@ -876,8 +884,16 @@ int search_rows(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds, c
     if (n_first < 1 || n_last < n_first) return fail(BNX_ERR_INVALID, "empty search domain");
     if ((kinds & 3u) == 0) return fail(BNX_ERR_INVALID, "kinds_mask selects no kind");
     TRY(activate(c));
-    TRY(prepare(c, n_last + 1, primes, np, plimit));
-    TRY(enqueue(c, n_first, n_last, kinds & 3u));
+    c->overlap_h2d = true;
+    const int rc = prepare(c, n_last + 1, primes, np, plimit);
+    c->overlap_h2d = false;
+    int rc2 = rc == BNX_OK ? enqueue(c, n_first, n_last, kinds & 3u) : rc;
+    if (c->h2d_pending) {  // the caller's buffer is read before the call returns
+        c->h2d_pending = false;
+        CK(cudaStreamWaitEvent(c->stream, c->h2d_ev, 0));
+        if (rc2 != BNX_OK) CK(cudaStreamSynchronize(c->aux));
+    }
+    TRY(rc2);
     return collect(c, rows);
 }
 
@@ -911,6 +927,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->h2d_ev, cudaEventDisableTiming));
     CK(heavy_configure());
     if (const char* env = std::getenv("BNX_GRAPHS")) c->use_graphs = std::atoi(env) != 0;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -973,6 +990,7 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
+    if (c->h2d_ev) cudaEventDestroy(c->h2d_ev);
     delete c;
     return BNX_OK;
 }
