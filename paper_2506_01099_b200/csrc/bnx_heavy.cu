@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + np2p);
     uint32_t* s_c32 = s_p + a.np2;
     __shared__ HeavyItem s_q[2 * T];
+    __shared__ uint64_t s_end[T];  // class ends of a multi-class window
     __shared__ int s_cnt;
     __shared__ unsigned long long s_cls;
     const int tid = threadIdx.x;
@@ -371,9 +372,28 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
             }
             const uint64_t w = base + tid;
             const uint64_t cls0 = s_cls;
+            // class of each item: the whole window in class cls0 (most windows), else the
+            // ends of the next T classes staged in shared memory and searched there
+            const bool one = (a.incl[cls0] & HEAVY_TRIAL_MASK) >= min(base + T, b1);  // CTA-uniform
+            if (!one) {
+                const uint64_t j = cls0 + tid;
+                s_end[tid] = j < a.nent ? (a.incl[j] & HEAVY_TRIAL_MASK) : ~0ull;
+                __syncthreads();
+            }
             uint64_t i = cls0;
             if (w < b1) {
-                i = first_class_above(a.incl, cls0, a.nent, w);
+                if (!one) {
+                    if (w < s_end[T - 1]) {
+                        int lo = 0, hi = T - 1;  // first staged class ending above w
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (s_end[mid] > w) hi = mid; else lo = mid + 1;
+                        }
+                        i = cls0 + lo;
+                    } else {
+                        i = first_class_above(a.incl, cls0 + T - 1, a.nent, w);
+                    }
+                }
                 const BnxHeavyEnt e = a.ent[i];
                 // item -> k: every k, or every odd k when sigma is even (see k_heavy_count)
                 const uint64_t k = a.klo[i] + ((w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0)) << (e.rmask & 1u));
