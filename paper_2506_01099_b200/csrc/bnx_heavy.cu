@@ -111,6 +111,27 @@ __device__ __forceinline__ bool twice_prod_ge(uint64_t sigma, uint64_t v, uint64
     return __umul64hi(s2, v) != 0 || s2 * v >= rhs;
 }
 
+// Trial classes list only the k that can be canonical as far as 2 and 3 go (gcd(k, sigma)
+// = 1): wsel = rmask & 3 = [2 | sigma] + 2 [3 | sigma] selects every k, the odd k, the k
+// not divisible by 3, or k = +-1 (mod 6).  wheel_rank(K) = listed k in [0, K]; wheel_k(rho)
+// = the listed k of rank rho (0-based, k = 0 listed only for wsel = 0).
+__device__ __forceinline__ uint64_t wheel_rank(uint64_t K, uint32_t wsel) {
+    switch (wsel) {
+        case 0: return K + 1;
+        case 1: return (K + 1) / 2;
+        case 2: return K - K / 3;
+        default: return 2 * (K / 6) + (K % 6 >= 1) + (K % 6 >= 5);
+    }
+}
+__device__ __forceinline__ uint64_t wheel_k(uint64_t rho, uint32_t wsel) {
+    switch (wsel) {
+        case 0: return rho;
+        case 1: return 2 * rho + 1;
+        case 2: return 3 * (rho >> 1) + 1 + (rho & 1);
+        default: return 6 * (rho >> 1) + 1 + 4 * (rho & 1);
+    }
+}
+
 __global__ void k_heavy_count(HeavyArgs a) {
     // the search's counters and flags start here (no memset launches; every later kernel
     // runs after this one)
@@ -144,14 +165,11 @@ __global__ void k_heavy_count(HeavyArgs a) {
             a.klo[i] = (uint32_t)ks;
             a.kcnt[i] = (uint32_t)cs;  // listed k (index space)
             continue;
-        } else if (e.rmask & 1u) {  // trial items; sigma even: only odd k can be canonical
-            const uint64_t ko = kl | 1u;
-            const uint64_t co = kh >= ko ? (kh - ko) / 2 + 1 : 0;
-            a.cnt[i] = co;
-            a.klo[i] = co ? (uint32_t)ko : 0u;
-        } else {
-            a.cnt[i] = c;
-            a.klo[i] = c ? (uint32_t)kl : 0u;
+        } else {  // trial items: the k coprime to 2 and 3 where sigma has them (wheel_k)
+            const uint32_t wsel = e.rmask & 3u;
+            const uint64_t r0 = wheel_rank(kl - 1, wsel);
+            a.cnt[i] = c ? wheel_rank(kh, wsel) - r0 : 0;
+            a.klo[i] = (uint32_t)r0;  // rank of the class's first item
         }
         a.kcnt[i] = 0;  // (sieve classes only)
     }
@@ -395,8 +413,8 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
                     }
                 }
                 const BnxHeavyEnt e = a.ent[i];
-                // item -> k: every k, or every odd k when sigma is even (see k_heavy_count)
-                const uint64_t k = a.klo[i] + ((w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0)) << (e.rmask & 1u));
+                // item -> k: the class's listed k (see wheel_k)
+                const uint64_t k = wheel_k(a.klo[i] + (w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0)), e.rmask & 3u);
                 if (k < a.nkinfo) {
                     bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
                     if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
