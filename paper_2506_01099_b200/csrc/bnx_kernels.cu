@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
     for (;;) {
         unsigned long long i = first;
         if (first == ~0ull) {
+            if (nwarps >= cnt) break;  // the static round covered every item
             if (lane == 0) i = nwarps + atomicAdd(&a.ctr[CTR_NEXT], 1ull);
             i = __shfl_sync(0xffffffffu, i, 0);
         }
