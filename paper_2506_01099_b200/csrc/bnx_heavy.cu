@@ -151,10 +151,12 @@ __global__ void k_heavy_count(HeavyArgs a) {
             while (top * e.b > a.x_hi) --top;
             while ((top + 1) * e.b <= a.x_hi) ++top;
             if (top < kh) kh = top;
-            uint64_t lo = (uint64_t)((double)a.x_lo * rb);
-            while (lo > 0 && lo * e.b >= a.x_lo) --lo;
-            while (lo * e.b < a.x_lo) ++lo;  // smallest lo with lo * b >= x_lo
-            if (lo > kl) kl = lo;
+            if (a.x_lo > e.b) {  // (else ceil(x_lo / b) = 1: every search from n = 1)
+                uint64_t lo = (uint64_t)((double)a.x_lo * rb);
+                while (lo > 0 && lo * e.b >= a.x_lo) --lo;
+                while (lo * e.b < a.x_lo) ++lo;  // smallest lo with lo * b >= x_lo
+                if (lo > kl) kl = lo;
+            }
         }
         const uint64_t c = kh >= kl ? kh - kl + 1 : 0;
         if (c >= a.kmin) {  // sieve chunks over every k (every odd k when sigma is even)
