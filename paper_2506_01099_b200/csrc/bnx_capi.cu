@@ -187,6 +187,7 @@ struct bnx_ctx {
     bnx_pair_t* pairs_p = nullptr;
     size_t pairs_cap = 0;
     unsigned char* h_io = nullptr;
+    uint64_t pair_prefix = PAIR_PREFIX;  // rows read back with the counters (BNX_PAIR_PREFIX: tests)
     unsigned long long* h_sctr = nullptr;
     int* h_sflags = nullptr;
     bnx_pair_t* h_pairs = nullptr;
@@ -519,7 +520,7 @@ int ensure_work(bnx_ctx* c) {
 // PAIR_PREFIX pair rows (every search up to 2^48 has fewer: 49 of both kinds), so collect()
 // needs no second copy.
 int read_back(bnx_ctx* c) {
-    CK(cudaMemcpyAsync(c->h_io, c->io.p, IO_PAIRS + sizeof(bnx_pair_t) * PAIR_PREFIX, cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(c->h_io, c->io.p, IO_PAIRS + sizeof(bnx_pair_t) * c->pair_prefix, cudaMemcpyDeviceToHost,
                        c->stream));
     return BNX_OK;
 }
@@ -850,7 +851,7 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
         }
         const uint64_t np = h[CTR_PAIRS];
         rows.resize(np);
-        if (np <= PAIR_PREFIX) {
+        if (np <= c->pair_prefix) {
             if (np) std::memcpy(rows.data(), c->h_pairs, sizeof(bnx_pair_t) * np);
         } else {
             CK(cudaMemcpyAsync(rows.data(), c->pairs_p, sizeof(bnx_pair_t) * np, cudaMemcpyDeviceToHost, c->stream));
@@ -938,6 +939,8 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_HEAVY_RUNS")) c->heavy_runs = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_RUN_FIRST")) c->heavy_run_first = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_KC")) c->heavy_kc = std::max(0, std::atoi(env)) & ~3;
+    if (const char* env = std::getenv("BNX_PAIR_PREFIX"))
+        c->pair_prefix = std::min<uint64_t>(PAIR_PREFIX, (uint64_t)std::max(0, std::atoi(env)));
     if (const char* env = std::getenv("BNX_TAIL_HEAVY")) c->tail_heavy = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_SCREEN_VARIANT")) {
         const int v = std::atoi(env);

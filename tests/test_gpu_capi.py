@@ -140,3 +140,26 @@ def test_graph_replay_follows_parameter_changes():
         c.set_stream(0)
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("prefix", ["0", "5"])
+def test_rows_beyond_the_read_back_prefix(prefix, golden):
+    """collect() returns the rows from the read-back copy when a search has at most
+    PAIR_PREFIX pairs, else with a second copy; a context started with a smaller prefix
+    (BNX_PAIR_PREFIX) takes the second path for the 33 pairs below 2^32."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = ("import json; from paper_2506_01099_b200 import _native; c = _native.Context(0); "
+            "r = c.search(2**32, 3, None, 0); print(json.dumps([[int(x['kind']), int(x['m']), int(x['n']), "
+            "int(x['rad_m']), int(x['rad_m1'])] for x in r]))")
+    env = dict(os.environ, BNX_PAIR_PREFIX=prefix)
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    exp = golden["expected_pairs_up_to"]["4294967296"]
+    assert json.loads(out.stdout.strip().splitlines()[-1]) == sorted(exp["first"] + exp["second"],
+                                                                      key=lambda r: (r[1], r[2]))
