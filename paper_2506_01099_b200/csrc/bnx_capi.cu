@@ -169,7 +169,7 @@ struct bnx_ctx {
     int heavy_grid = 0;       // tuning only (BNX_HEAVY_GRID, CTAs per SM); 0 = default
     int heavy_runs = -1;      // tuning only (BNX_HEAVY_RUNS, fetched screen runs per CTA); -1 = default
     int heavy_run_first = -1; // tuning only (BNX_HEAVY_RUN_FIRST, static share /256); -1 = default
-    int heavy_kc = 0;         // tuning only (BNX_HEAVY_KC, k per sieve chunk, multiple of 4); 0 = default
+    int heavy_kc = 0;         // tuning only (BNX_HEAVY_KC, k per sieve chunk, multiple of 8); 0 = default
     uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
     DBuf<ulonglong2> q1;
@@ -938,7 +938,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_HEAVY_GRID")) c->heavy_grid = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_RUNS")) c->heavy_runs = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_RUN_FIRST")) c->heavy_run_first = std::max(0, std::atoi(env));
-    if (const char* env = std::getenv("BNX_HEAVY_KC")) c->heavy_kc = std::max(0, std::atoi(env)) & ~3;
+    if (const char* env = std::getenv("BNX_HEAVY_KC")) c->heavy_kc = std::max(0, std::atoi(env)) & ~7;
     if (const char* env = std::getenv("BNX_PAIR_PREFIX"))
         c->pair_prefix = std::min<uint64_t>(PAIR_PREFIX, (uint64_t)std::max(0, std::atoi(env)));
     if (const char* env = std::getenv("BNX_TAIL_HEAVY")) c->tail_heavy = std::strtoull(env, nullptr, 10);
