@@ -153,6 +153,7 @@ struct bnx_ctx {
     int screen_v = 0;
     int screen_skip = 0;  // profiling only
     int sieve_blocks_per_sm = 1;
+    int sieve_v = 0;
 
     // prime table (device u32 + host mirror)
     DBuf<uint32_t> primes;
@@ -951,9 +952,15 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
         CK(cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sv.smem));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->screen_blocks_per_sm, sv.fn, sv.threads, sv.smem));
     }
-    CK(cudaFuncSetAttribute(sieve_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sieve_smem_bytes()));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_blocks_per_sm, sieve_kernel(), SIEVE_THREADS,
-                                                     sieve_smem_bytes()));
+    if (const char* env = std::getenv("BNX_SIEVE_VARIANT")) {
+        const int v = std::atoi(env);
+        if (v >= 0 && v < sieve_variant_count()) c->sieve_v = v;
+    }
+    {
+        const SieveVariant& sv = sieve_variant(c->sieve_v);
+        CK(cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sv.smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_blocks_per_sm, sv.fn, sv.threads, sv.smem));
+    }
     c->screen_blocks_per_sm = std::max(1, c->screen_blocks_per_sm);
     c->sieve_blocks_per_sm = std::max(1, c->sieve_blocks_per_sm);
     *out = c;
@@ -1079,14 +1086,15 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
     const uint64_t end = start + (length - 1);
     const uint64_t need = isqrt_u64(end);
     TRY(ensure_primes(c, primes, np, plimit, need));
-    TRY(build_tables(c, c->sieve_tab, end, fast ? 0 : 1, SIEVE_TILE, SIEVE_THREADS / 32));
+    const SieveVariant& sv = sieve_variant(c->sieve_v);
+    TRY(build_tables(c, c->sieve_tab, end, fast ? 0 : 1, (uint32_t)sv.tile, sv.threads / 32));
     if (c->sieve_tab.nsmall > (uint32_t)SIEVE_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     TRY(c->flags.ensure(4));
     if (!c->h_flags) CK(cudaMallocHost(&c->h_flags, sizeof(int) * 4));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
     const uint64_t piece = out_dev ? length : std::min<uint64_t>(length, 1ull << 27);
     if (!out_dev) TRY(c->sieve_out.ensure(piece));
-    const uint64_t SEG = (uint64_t)SIEVE_TILE * SIEVE_NT;
+    const uint64_t SEG = (uint64_t)sv.tile * sv.nt;
     for (uint64_t off = 0; off < length; off += piece) {
         const uint64_t len = std::min<uint64_t>(piece, length - off);
         uint64_t* dst = out_dev ? out_dev : c->sieve_out.p;
@@ -1094,7 +1102,7 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
                      c->sieve_tab.nlarge, c->sieve_tab.items.p, c->sieve_tab.nitems, fast, dst, c->flags.p};
         const uint64_t nseg = (len + SEG - 1) / SEG;
         const int grid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->sieve_blocks_per_sm);
-        launch_sieve(sa, grid, c->stream);
+        sv.launch(sa, grid, c->stream);
         CK(cudaGetLastError());
         if (!out_dev) CK(cudaMemcpyAsync(out_host + off, dst, sizeof(uint64_t) * len, cudaMemcpyDeviceToHost, c->stream));
     }

@@ -518,8 +518,8 @@ __device__ __forceinline__ void div_slot(unsigned long long* s, uint64_t inv, bo
     } while (old != assumed);
 }
 
-template <int TILE, int NT, int THREADS, int BCAP, int MAXS>
-__global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
+template <int TILE, int NT, int THREADS, int BCAP, int MAXS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
     constexpr int NW = THREADS / 32;
     constexpr uint64_t SEG = (uint64_t)TILE * NT;
     extern __shared__ __align__(16) unsigned long long sm64[];
@@ -631,8 +631,12 @@ __global__ void __launch_bounds__(THREADS, 2) k_sieve_exact(SieveArgs a) {
                     __stcs(reinterpret_cast<ulonglong2*>(dst) + g, reinterpret_cast<const ulonglong2*>(r)[g]);
                     if (next) init_pair(a.start + toff + TILE, g);
                 }
-            } else {
-                for (int i = tid; i < lim; i += THREADS) dst[i] = r[i];
+            } else {  // ragged last tile or an output only 8-byte aligned: same slot ownership
+                for (int g = tid; g < TILE / 2; g += THREADS) {
+                    if (2 * g < lim) dst[2 * g] = r[2 * g];
+                    if (2 * g + 1 < lim) dst[2 * g + 1] = r[2 * g + 1];
+                    if (next) init_pair(a.start + toff + TILE, g);
+                }
             }
         }
     }
@@ -765,14 +769,28 @@ __global__ void k_table_probe(TableArgs a) {
 
 // ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
-size_t sieve_smem_bytes() {
-    return sizeof(unsigned long long) * ((size_t)SIEVE_TILE + (size_t)SIEVE_NT * SIEVE_BCAP + SIEVE_MAXS) +
-           sizeof(uint32_t) * ((size_t)SIEVE_NT + 5 * SIEVE_MAXS);
+template <int TILE, int NT, int BCAP>
+constexpr size_t sieve_smem() {
+    return sizeof(unsigned long long) * ((size_t)TILE + (size_t)NT * BCAP + SIEVE_MAXS) +
+           sizeof(uint32_t) * ((size_t)NT + 5 * SIEVE_MAXS);
 }
-
-const void* sieve_kernel() {
-    return (const void*)k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>;
+template <int TILE, int NT, int THREADS, int BCAP, int MINB>
+void launch_sieve_v(const SieveArgs& a, int grid, cudaStream_t st) {
+    k_sieve_exact<TILE, NT, THREADS, BCAP, SIEVE_MAXS, MINB><<<grid, THREADS, sieve_smem<TILE, NT, BCAP>(), st>>>(a);
 }
+#define BNX_SIEVE_VARIANT(T, N, H, B, M)                                                                   \
+    SieveVariant{T, N, H, B, (const void*)k_sieve_exact<T, N, H, B, SIEVE_MAXS, M>, sieve_smem<T, N, B>(), \
+                 launch_sieve_v<T, N, H, B, M>}
+static const SieveVariant kSieveVariants[] = {
+    // default; the others measured slower on [1, 2^30] (scripts/sieve_variants.py,
+    // profiles/r01_sieve_variants.jsonl): 2.18 ms against 2.44, 2.62, 2.78
+    BNX_SIEVE_VARIANT(SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, 2),
+    BNX_SIEVE_VARIANT(8192, 64, 768, 64, 2),
+    BNX_SIEVE_VARIANT(8192, 64, 256, 64, 4),
+    BNX_SIEVE_VARIANT(4096, 64, 512, 48, 3),
+};
+int sieve_variant_count() { return (int)(sizeof(kSieveVariants) / sizeof(kSieveVariants[0])); }
+const SieveVariant& sieve_variant(int i) { return kSieveVariants[i]; }
 
 template <int TILE, int NT, int THREADS, int BCAP>
 constexpr size_t screen_smem() {
@@ -795,10 +813,6 @@ static const ScreenVariant kScreenVariants[] = {
 };
 int screen_variant_count() { return (int)(sizeof(kScreenVariants) / sizeof(kScreenVariants[0])); }
 const ScreenVariant& screen_variant(int i) { return kScreenVariants[i]; }
-void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st) {
-    k_sieve_exact<SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, SIEVE_MAXS>
-        <<<grid, SIEVE_THREADS, sieve_smem_bytes(), st>>>(a);
-}
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
     k_tail<<<grid, 256, 0, st>>>(a);
     k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);

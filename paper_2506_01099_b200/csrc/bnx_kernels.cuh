@@ -163,9 +163,16 @@ struct TableArgs {
 };
 void launch_table_insert(const TableArgs& a, int grid, cudaStream_t st);
 void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st);
-size_t sieve_smem_bytes();
-const void* sieve_kernel();
-void launch_sieve(const SieveArgs& a, int grid, cudaStream_t st);
+// Compiled exact-sieve geometries (tile, tiles per segment, threads, bucket capacity); the
+// context picks one at creation (BNX_SIEVE_VARIANT, default 0).
+struct SieveVariant {
+    int tile, nt, threads, bcap;
+    const void* fn;
+    size_t smem;
+    void (*launch)(const SieveArgs&, int, cudaStream_t);
+};
+int sieve_variant_count();
+const SieveVariant& sieve_variant(int i);
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st);
 void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st, bool pdl = false);  // heavy engine: k_tail only
 void launch_tail_heavy(const TailArgs& a, cudaStream_t st);            // heavy engine: k_tail_heavy only

@@ -87,6 +87,29 @@ def test_torch_stream_and_device_sieve():
         ctx.close()
 
 
+@pytest.mark.parametrize("start,length", [(987654321, (1 << 20) + 12345), (3, 777), (2**40 - 5, 70_001)])
+def test_device_sieve_unaligned_output(start, length):
+    """bnx_sieve_radicals_dev into a pointer that is 8- but not 16-byte aligned (a tensor
+    view at an odd element offset): every tile of every segment must still be initialised
+    (the 16-byte store path is skipped), ragged lengths included."""
+    torch = pytest.importorskip("torch")
+    from oracle import oracle as orc
+    import paper_2506_01099_b200 as pkg
+
+    ctx = _native.Context(0)
+    try:
+        buf = torch.full((length + 2,), -1, dtype=torch.int64, device="cuda")
+        ctx.sieve_radicals_dev(start, length, buf.data_ptr() + 8)
+        torch.cuda.synchronize()
+        got = buf.cpu().numpy().view(np.uint64)
+        iv = pkg.Interval(start, length)
+        want = orc.sieve_segment(start, length, orc.primes_up_to(pkg.required_prime_bound(iv)))
+        assert np.array_equal(got[1 : length + 1], want)
+        assert got[0] == np.uint64(2**64 - 1) and got[length + 1] == np.uint64(2**64 - 1)  # no stray writes
+    finally:
+        ctx.close()
+
+
 def test_domain_search_equals_filtered_full(L, ctx):
     found = ctypes.c_size_t(0)
     buf = (_native.PairRow * 64)()
