@@ -129,7 +129,9 @@ BNX_API int bnx_primes_up_to(bnx_ctx_t* ctx, uint64_t limit, uint64_t* out, size
  * BNX_ERR_PRIMES_UNCOVERED when primes_limit < isqrt(start + length - 1). */
 BNX_API int bnx_sieve_radicals(bnx_ctx_t* ctx, uint64_t start, uint64_t length, const uint64_t* primes,
                        size_t nprimes, uint64_t primes_limit, int ctz_fast_path, uint64_t* out);
-/* Same, writing into device memory `out_dev` on the context stream (no host sync). */
+/* Same, writing into device memory `out_dev` (any 8-byte aligned pointer) on the context
+ * stream, with the device prime table; no host copy of the radicals.  The call waits for
+ * the stream once at the end to read the bucket-overflow flag. */
 BNX_API int bnx_sieve_radicals_dev(bnx_ctx_t* ctx, uint64_t start, uint64_t length, int ctz_fast_path,
                            uint64_t* out_dev);
 

@@ -1120,6 +1120,7 @@ int bnx_sieve_radicals(bnx_ctx_t* c, uint64_t start, uint64_t length, const uint
 
 int bnx_sieve_radicals_dev(bnx_ctx_t* c, uint64_t start, uint64_t length, int ctz_fast_path, uint64_t* out_dev) {
     if (!c || !out_dev) return fail(BNX_ERR_INVALID, "null argument");
+    if (((uintptr_t)out_dev) & 7) return fail(BNX_ERR_INVALID, "out_dev must be 8-byte aligned");
     return sieve_common(c, start, length, nullptr, 0, 0, ctz_fast_path, nullptr, out_dev);
 }
 

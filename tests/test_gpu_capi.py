@@ -106,6 +106,8 @@ def test_device_sieve_unaligned_output(start, length):
         want = orc.sieve_segment(start, length, orc.primes_up_to(pkg.required_prime_bound(iv)))
         assert np.array_equal(got[1 : length + 1], want)
         assert got[0] == np.uint64(2**64 - 1) and got[length + 1] == np.uint64(2**64 - 1)  # no stray writes
+        with pytest.raises(ValueError, match="aligned"):
+            ctx.sieve_radicals_dev(start, 16, buf.data_ptr() + 4)
     finally:
         ctx.close()
 
