@@ -87,8 +87,9 @@ def test_torch_stream_and_device_sieve():
         ctx.close()
 
 
+@pytest.mark.parametrize("ctz", [True, False])
 @pytest.mark.parametrize("start,length", [(987654321, (1 << 20) + 12345), (3, 777), (2**40 - 5, 70_001)])
-def test_device_sieve_unaligned_output(start, length):
+def test_device_sieve_unaligned_output(start, length, ctz):
     """bnx_sieve_radicals_dev into a pointer that is 8- but not 16-byte aligned (a tensor
     view at an odd element offset): every tile of every segment must still be initialised
     (the 16-byte store path is skipped), ragged lengths included."""
@@ -99,7 +100,7 @@ def test_device_sieve_unaligned_output(start, length):
     ctx = _native.Context(0)
     try:
         buf = torch.full((length + 2,), -1, dtype=torch.int64, device="cuda")
-        ctx.sieve_radicals_dev(start, length, buf.data_ptr() + 8)
+        ctx.sieve_radicals_dev(start, length, buf.data_ptr() + 8, ctz_fast_path=ctz)
         torch.cuda.synchronize()
         got = buf.cpu().numpy().view(np.uint64)
         iv = pkg.Interval(start, length)
