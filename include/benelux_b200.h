@@ -100,10 +100,15 @@ BNX_API int bnx_ctx_create(int device, bnx_ctx_t** out);
 BNX_API int bnx_ctx_destroy(bnx_ctx_t* ctx);
 BNX_API int bnx_ctx_set_stream(bnx_ctx_t* ctx, void* stream);
 BNX_API int bnx_ctx_stats(const bnx_ctx_t* ctx, bnx_stats_t* out);
-/* Kernel timing with CUDA events on the context stream: when enabled, each search records
+/* Kernel timing with CUDA events on the context stream: with mode 1, each search records
  * events around the candidate generator (screen) and around the whole device pipeline; bnx_ctx_timing
- * returns the last search's milliseconds (valid after bnx_search_collect / bnx_search*). */
-BNX_API int bnx_ctx_set_timing(bnx_ctx_t* ctx, int enabled);
+ * returns the last search's milliseconds (valid after bnx_search_collect / bnx_search*).  Mode 2
+ * launches the heavy engine's kernels directly (no graph, no programmatic overlap) with events
+ * between them; bnx_ctx_kernel_timing returns up to 4 stage times in ms: [0] k_heavy_count + scan,
+ * [1] k_heavy_screen (with k_heavy_sieve beside it above ~2^33), [2] k_heavy_exact, [3] the tail.
+ * Mode 0 (default) records nothing. */
+BNX_API int bnx_ctx_set_timing(bnx_ctx_t* ctx, int mode);
+BNX_API int bnx_ctx_kernel_timing(const bnx_ctx_t* ctx, float* ms, int n);
 /* Candidate generator of the search (results are identical):
  * BNX_ENGINE_HEAVY (default) lists the heavy integers (2 s(x)^2 >= x, s = x / rad x) and tests
  * their neighbours; BNX_ENGINE_SCREEN sieves a log-surplus byte per integer.  The environment
@@ -163,7 +168,8 @@ BNX_API int bnx_search_domain(bnx_ctx_t* ctx, uint64_t n_first, uint64_t n_last,
 
 /* Split-phase form for timing: enqueue the whole search on the context stream without a
  * host sync (device-resident prime tables must already exist: call bnx_prepare first),
- * then collect.  bnx_prepare builds / uploads the tables for bound `max_x`. */
+ * then collect.  bnx_prepare builds / uploads the tables for bound `max_x`.  A collect that
+ * returns BNX_BUFFER_FULL keeps the rows: call it again with a buffer of *found rows. */
 BNX_API int bnx_prepare(bnx_ctx_t* ctx, uint64_t max_x, const uint64_t* primes, size_t nprimes,
                 uint64_t primes_limit);
 BNX_API int bnx_search_enqueue(bnx_ctx_t* ctx, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask);

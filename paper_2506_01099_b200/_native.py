@@ -29,7 +29,7 @@ ENGINES = {"heavy": 0, "screen": 1}  # bnx_ctx_set_engine (include/benelux_b200.
 # Every symbol include/benelux_b200.h declares (tests check the library exports them all).
 EXPORTED_SYMBOLS = (
     "bnx_version", "bnx_last_error", "bnx_device_count", "bnx_ctx_create", "bnx_ctx_destroy",
-    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_ctx_set_shard", "bnx_primes_up_to", "bnx_sieve_radicals",
+    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_kernel_timing", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_ctx_set_shard", "bnx_primes_up_to", "bnx_sieve_radicals",
     "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain", "bnx_search_multi",
     "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of", "bnx_brute_force",
     "bnx_table_create", "bnx_table_destroy", "bnx_table_insert_all", "bnx_table_probe_all", "bnx_table_slots",
@@ -114,6 +114,7 @@ def load() -> ctypes.CDLL:
         L.bnx_ctx_engine.argtypes = [vp]
         L.bnx_ctx_set_shard.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32]
         L.bnx_ctx_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
+        L.bnx_ctx_kernel_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
         L.bnx_primes_up_to.argtypes = [vp, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_sieve_radicals.argtypes = [
             vp, ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int, _u64p,
@@ -199,9 +200,10 @@ class Context:
         check(load().bnx_ctx_stats(self.handle, ctypes.byref(s)))
         return s.as_dict()
 
-    def set_timing(self, enabled: bool) -> None:
+    def set_timing(self, mode: bool | int) -> None:
+        """0/False: off; 1/True: generator / pipeline split; 2: per-kernel events (direct launches)."""
         with self.lock:
-            check(load().bnx_ctx_set_timing(self.handle, int(bool(enabled))))
+            check(load().bnx_ctx_set_timing(self.handle, int(mode)))
 
     def set_engine(self, engine: str | int) -> None:
         """Candidate generator: "heavy" (default) or "screen" (identical results)."""
@@ -223,6 +225,12 @@ class Context:
         a, b = ctypes.c_float(0), ctypes.c_float(0)
         check(load().bnx_ctx_timing(self.handle, ctypes.byref(a), ctypes.byref(b)))
         return float(a.value), float(b.value)
+
+    def kernel_timing(self) -> dict:
+        """Per-stage ms of the last search in timing mode 2 (include/benelux_b200.h)."""
+        ms = (ctypes.c_float * 4)()
+        check(load().bnx_ctx_kernel_timing(self.handle, ms, 4))
+        return dict(zip(("count_scan", "screen", "exact", "tail"), (float(v) for v in ms)))
 
     # -- primes ---------------------------------------------------------------------
     def primes_up_to(self, limit: int) -> np.ndarray:

@@ -200,9 +200,16 @@ struct bnx_ctx {
     DBuf<uint64_t> sieve_out;
 
     // optional event timing of the pipeline
-    bool timing = false;
+    int timing = 0;  // 1: generator / pipeline split (two graphs); 2: per-kernel events, direct launches
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t kev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     float screen_ms = 0.f, pipeline_ms = 0.f;
+    float kernel_ms[4] = {0.f, 0.f, 0.f, 0.f};  // count + scan, screen (+ sieve), exact, tail
+
+    // rows of a collected search the caller's buffer could not take (bnx_search_collect
+    // returns them again on the next call instead of losing them)
+    bool rows_pending = false;
+    std::vector<bnx_pair_t> pending;
 
     // the enqueued search
     bool q_valid = false;
@@ -438,30 +445,50 @@ int build_heavy(bnx_ctx* c, uint64_t max_x) {
     if (P.empty() || (P.back() < root && c->primes_limit < root))
         return fail(BNX_ERR_PRIMES_UNCOVERED, "prime table does not cover sqrt(bound)");
     std::vector<BnxHeavyEnt> ents;
+    std::vector<uint64_t> vkey;  // (experiment, BNX_HEAVY_ORDER=2) v of b = u^2 v^3, v squarefree
     ents.reserve((size_t)(2.5 * std::sqrt((double)max_x)) + 64);
-    struct Node { uint64_t b, sigma, r; uint32_t rmask, rbig, rbig_min; size_t next; };
+    struct Node { uint64_t b, sigma, r; uint32_t rmask, rbig, rbig_min; size_t next; uint64_t v; };
     std::vector<Node> stack;
-    stack.push_back(Node{1, 1, 1, 0, 1, 0, 0});
+    stack.push_back(Node{1, 1, 1, 0, 1, 0, 0, 1});
     while (!stack.empty()) {
         const Node f = stack.back();
         stack.pop_back();
         ents.push_back(BnxHeavyEnt{f.b, f.sigma / f.r, (uint32_t)f.r, f.rmask, f.rbig, f.rbig_min});
+        vkey.push_back(f.v);
         for (size_t i = f.next; i < P.size(); ++i) {
             const uint64_t p = P[i];
             if (p > root || f.b > max_x / (p * p)) break;
-            Node ch{f.b * p * p, f.sigma * p, f.r * p, f.rmask, f.rbig, f.rbig_min, i + 1};
+            Node ch{f.b * p * p, f.sigma * p, f.r * p, f.rmask, f.rbig, f.rbig_min, i + 1, f.v};
             if (i < 31) ch.rmask |= 1u << i;
             else {
                 ch.rbig = (uint32_t)(f.rbig * p);
                 if (!ch.rbig_min) ch.rbig_min = (uint32_t)p;
             }
+            bool odd = false;
             for (;;) {
                 stack.push_back(ch);
                 if (ch.b > max_x / p) break;
                 ch.b *= p;
                 ch.sigma *= p;
+                odd = !odd;
+                ch.v = odd ? f.v * p : f.v;
             }
         }
+    }
+    if (const char* env = std::getenv("BNX_HEAVY_ORDER")) {  // class-order experiment
+        const int order = std::atoi(env);
+        std::vector<size_t> idx(ents.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+        auto ukey = [&](size_t i) { return (uint64_t)std::llround(std::sqrt((double)(ents[i].b / (vkey[i] * vkey[i] * vkey[i])))); };
+        if (order == 1) std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return ents[a].b < ents[b].b; });
+        if (order == 2)
+            std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+                return vkey[a] != vkey[b] ? vkey[a] < vkey[b] : ukey(a) < ukey(b);
+            });
+        if (order == 3) std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return ents[a].b > ents[b].b; });
+        std::vector<BnxHeavyEnt> sorted(ents.size());
+        for (size_t i = 0; i < idx.size(); ++i) sorted[i] = ents[idx[i]];
+        ents.swap(sorted);
     }
     // (kept in DFS order: classes of one prime structure stay together, which measured ~10%
     // faster at 2^32 than sorting by sigma, and the host sort cost 0.35 s at 2^40, 7 s at 2^48;
@@ -670,7 +697,8 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
             CK(cudaMemsetAsync(c->ctr_p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
             CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
         }
-        launch_heavy(ha, h.scan_temp.p, h.scan_bytes, grid, c->stream, nullptr, c->aux, c->fork_ev, c->join_ev);
+        launch_heavy(ha, h.scan_temp.p, h.scan_bytes, grid, c->stream, nullptr, c->aux, c->fork_ev, c->join_ev,
+                     c->timing == 2 ? c->kev : nullptr);
         CK(cudaGetLastError());
         return BNX_OK;
     };
@@ -688,12 +716,13 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         CK(cudaGetLastError());
         return read_back(c);
     };
-    if (!c->use_graphs) {
+    if (!c->use_graphs || c->timing == 2) {
         if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
         TRY(record_gen());
         if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
         TRY(record_tail());
         if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+        if (c->timing == 2) CK(cudaEventRecord(c->kev[4], c->stream));
     } else {
         // two graph launches replay the whole search (about ten stream operations): the host
         // enqueue cost and the inter-kernel gaps go; re-captured when any parameter changes
@@ -868,6 +897,8 @@ int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
             CK(cudaEventElapsedTime(&c->screen_ms, c->ev[0], c->ev[1]));
             CK(cudaEventElapsedTime(&c->pipeline_ms, c->ev[0], c->ev[2]));
         }
+        if (c->timing == 2 && c->engine == 0)
+            for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(&c->kernel_ms[i], c->kev[i], c->kev[i + 1]));
         c->q_valid = false;
         return BNX_OK;
     }
@@ -990,6 +1021,8 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->sieve_out.release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : c->kev)
+        if (e) cudaEventDestroy(e);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->h_io) cudaFreeHost(c->h_io);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1031,10 +1064,20 @@ int bnx_ctx_stats(const bnx_ctx_t* c, bnx_stats_t* out) {
 int bnx_ctx_set_timing(bnx_ctx_t* c, int enabled) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");
     TRY(activate(c));
+    if (enabled < 0 || enabled > 2) return fail(BNX_ERR_INVALID, "timing mode must be 0, 1 or 2");
     if (enabled)
         for (auto& e : c->ev)
             if (!e) CK(cudaEventCreate(&e));
-    c->timing = enabled != 0;
+    if (enabled == 2)
+        for (auto& e : c->kev)
+            if (!e) CK(cudaEventCreate(&e));
+    c->timing = enabled;
+    return BNX_OK;
+}
+
+int bnx_ctx_kernel_timing(const bnx_ctx_t* c, float* ms, int n) {
+    if (!c || !ms) return fail(BNX_ERR_INVALID, "null argument");
+    for (int i = 0; i < n && i < 4; ++i) ms[i] = c->kernel_ms[i];
     return BNX_OK;
 }
 
@@ -1191,6 +1234,8 @@ int bnx_prepare(bnx_ctx_t* c, uint64_t max_x, const uint64_t* primes, size_t npr
 int bnx_search_enqueue(bnx_ctx_t* c, uint64_t n_first, uint64_t n_last, uint32_t kinds_mask) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");
     if (n_first < 1 || n_last < n_first) return fail(BNX_ERR_INVALID, "empty search domain");
+    c->rows_pending = false;  // a new search drops rows nobody collected
+    c->pending.clear();
     if (c->screen_tab.gen != c->gen || c->screen_tab.max_x < n_last + 1)  // prepared for a large enough bound
         return fail(BNX_ERR_INVALID, "bnx_prepare must cover n_last + 1 first");
     TRY(activate(c));
@@ -1200,12 +1245,25 @@ int bnx_search_enqueue(bnx_ctx_t* c, uint64_t n_first, uint64_t n_last, uint32_t
 int bnx_search_collect(bnx_ctx_t* c, bnx_pair_t* out, size_t cap, size_t* found) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");
     TRY(activate(c));
+    if (c->rows_pending) {  // a retry after BNX_BUFFER_FULL
+        const int r = emit(c->pending, out, cap, found);
+        if (r == BNX_OK) {
+            c->rows_pending = false;
+            c->pending.clear();
+        }
+        return r;
+    }
     std::vector<bnx_pair_t> rows;
     TRY(collect(c, rows));
     std::sort(rows.begin(), rows.end(), [](const bnx_pair_t& a, const bnx_pair_t& b) {
         return a.n != b.n ? a.n < b.n : a.m < b.m;
     });
-    return emit(rows, out, cap, found);
+    const int r = emit(rows, out, cap, found);
+    if (r == BNX_BUFFER_FULL) {
+        c->pending.swap(rows);
+        c->rows_pending = true;
+    }
+    return r;
 }
 
 int bnx_search(bnx_ctx_t* c, uint64_t limit, uint32_t kinds_mask, const uint64_t* primes, size_t nprimes,

@@ -806,8 +806,10 @@ size_t heavy_scan_temp_bytes(uint64_t nent) {
 }
 
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
-                  cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+                  cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join,
+                  const cudaEvent_t* kev) {
     bool pdl = false;
+    if (kev) cudaEventRecord(kev[0], st);
     if (a.nent) {
         const unsigned cb = (unsigned)std::min<uint64_t>((a.nent + 255) / 256, 4096);
         k_heavy_count<<<cb, 256, 0, st>>>(a);
@@ -824,10 +826,14 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         const size_t np2p = (size_t)(a.np2 + 31) & ~(size_t)31;  // (see k_heavy_screen)
         const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint32_t)) +
                              np2p * (sizeof(uint2) + sizeof(uint32_t));
+        if (kev) cudaEventRecord(kev[1], st);
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
-        pdl = !sieve;
+        pdl = !sieve && !kev;
+    } else if (kev) {
+        cudaEventRecord(kev[1], st);
     }
+    if (kev) cudaEventRecord(kev[2], st);
     const size_t np3p = (size_t)(a.np3 + 31) & ~(size_t)31;  // (see k_heavy_exact)
     const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t)) + np3p * (sizeof(uint2) + sizeof(uint32_t));
     {  // a programmatic dependent launch right after k_heavy_screen (see k_heavy_exact)
@@ -843,6 +849,7 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         cfg.numAttrs = pdl ? 1 : 0;
         cudaLaunchKernelEx(&cfg, k_heavy_exact, a);
     }
+    if (kev) cudaEventRecord(kev[3], st);
     if (ev_generated) cudaEventRecord(ev_generated, st);
 }
 

@@ -117,7 +117,8 @@ void launch_pdiv32(const BnxPDiv* pdiv, uint64_t n, uint4* out, cudaStream_t st)
 cudaError_t heavy_configure();
 size_t heavy_sieve_smem(int np2, int kc, int ntasks);
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
-                  cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join);
+                  cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join,
+                  const cudaEvent_t* kev = nullptr);  // kev[0..3]: per-kernel timing (count, screen, exact)
 
 struct SieveArgs {
     uint64_t start, length;

@@ -343,3 +343,52 @@ def test_repeated_searches_are_identical():
         st = ctx.stats()
         assert (st["survivors"], st["candidates"], st["matches"]) == \
             (ref_st["survivors"], ref_st["candidates"], ref_st["matches"])
+
+
+# ------------------------------------------- BASELINE configs[3] / configs[4] at full size ----
+def _rows(pairs):
+    return [(int(p.kind), p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in pairs]
+
+
+def test_paper_range_both_kinds_is_theorem_1():
+    """configs[4]: every pair of both kinds below 1.4e12 in one device search -- exactly the
+    42 rows of Theorem 1, radicals included."""
+    from oracle import theorem1
+
+    S = theorem1.COMPLETENESS_BOUND
+    want = theorem1.known_rows(S)
+    assert len(want) == 42
+    assert _rows(bp.find_pairs_sorted(S)) == want
+    for kind in (1, 2):
+        got = _rows(bp.search.find_pairs(S, kinds=kind))
+        assert got == [r for r in want if r[0] == kind], kind
+
+
+@pytest.mark.parametrize("nshards", [2, 4, 8])
+def test_multi_gpu_shards_paper_range(nshards):
+    """configs[3]/[4] through the multi-device entry point (bnx_search_multi): `nshards`
+    item shards (here all on cuda:0) below 2^40 (first kind) and below 1.4e12 (both kinds)
+    merge to exactly Theorem 1."""
+    from oracle import theorem1
+
+    S40 = 1 << 40
+    got = _rows(bp.find_pairs_multi_gpu(S40, [0] * nshards, kinds=1))
+    assert got == [r for r in theorem1.known_rows(S40) if r[0] == 1]
+    assert len(got) == 20
+    S = theorem1.COMPLETENESS_BOUND
+    assert _rows(bp.find_pairs_multi_gpu(S, [0] * nshards)) == theorem1.known_rows(S)
+
+
+def test_item_shards_strong_config_partition():
+    """configs[3]'s per-rank work (bench.py --gpus N): the 8 item shards of the first-kind
+    search below 2^40 are disjoint and their union is the unsharded search."""
+    ctx = bp._native.context(None)
+    full = sorted(map(tuple, bp.search.search_rows(1, 2**40 - 1, kinds=1).tolist()))
+    parts = []
+    try:
+        for sh in range(8):
+            ctx.set_shard(sh, 8)
+            parts += list(map(tuple, bp.search.search_rows(1, 2**40 - 1, kinds=1).tolist()))
+    finally:
+        ctx.set_shard(0, 1)
+    assert sorted(parts) == full and len(full) == 20
