@@ -414,7 +414,7 @@ def run_ours(args) -> None:
             a, b = search_shard(0, k)
             rows_s = ctx.collect()
             sms.append(a.elapsed_time(b))
-            same &= [(int(r["m"]), int(r["n"])) for r in rows_s] == exp_keys
+            same &= sorted((int(r["m"]), int(r["n"])) for r in rows_s) == exp_keys
         ctx.set_engine("heavy")
         screen_engine = {"engine": "screen (k_screen: one byte per integer, every integer visited)",
                          "ms_per_step": sum(sms) / len(sms), "value": (S - 1) / (sum(sms) / len(sms) / 1e3),
