@@ -109,6 +109,11 @@ BNX_API int bnx_ctx_stats(const bnx_ctx_t* ctx, bnx_stats_t* out);
  * Mode 0 (default) records nothing. */
 BNX_API int bnx_ctx_set_timing(bnx_ctx_t* ctx, int mode);
 BNX_API int bnx_ctx_kernel_timing(const bnx_ctx_t* ctx, float* ms, int n);
+/* Diagnostics (tests): prepare for bound max_x and copy out the heavy generator's surplus-class
+ * table in its device order: b_out[i] = b, m_out[i] = m | r << 40 (either may be NULL).
+ * *count receives the class count; BNX_BUFFER_FULL if it exceeds cap. */
+BNX_API int bnx_ctx_class_table(bnx_ctx_t* ctx, uint64_t max_x, uint64_t* b_out, uint64_t* m_out, size_t cap,
+                                size_t* count);
 /* Candidate generator of the search (results are identical):
  * BNX_ENGINE_HEAVY (default) lists the heavy integers (2 s(x)^2 >= x, s = x / rad x) and tests
  * their neighbours; BNX_ENGINE_SCREEN sieves a log-surplus byte per integer.  The environment

@@ -29,7 +29,7 @@ ENGINES = {"heavy": 0, "screen": 1}  # bnx_ctx_set_engine (include/benelux_b200.
 # Every symbol include/benelux_b200.h declares (tests check the library exports them all).
 EXPORTED_SYMBOLS = (
     "bnx_version", "bnx_last_error", "bnx_device_count", "bnx_ctx_create", "bnx_ctx_destroy",
-    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_kernel_timing", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_ctx_set_shard", "bnx_primes_up_to", "bnx_sieve_radicals",
+    "bnx_ctx_set_stream", "bnx_ctx_stats", "bnx_ctx_set_timing", "bnx_ctx_timing", "bnx_ctx_kernel_timing", "bnx_ctx_class_table", "bnx_ctx_set_engine", "bnx_ctx_engine", "bnx_ctx_set_shard", "bnx_primes_up_to", "bnx_sieve_radicals",
     "bnx_sieve_radicals_dev", "bnx_radicals_trial_division", "bnx_search", "bnx_search_domain", "bnx_search_multi",
     "bnx_prepare", "bnx_search_enqueue", "bnx_search_collect", "bnx_slot_of", "bnx_brute_force",
     "bnx_table_create", "bnx_table_destroy", "bnx_table_insert_all", "bnx_table_probe_all", "bnx_table_slots",
@@ -115,6 +115,8 @@ def load() -> ctypes.CDLL:
         L.bnx_ctx_set_shard.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32]
         L.bnx_ctx_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
         L.bnx_ctx_kernel_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+        L.bnx_ctx_class_table.argtypes = [vp, ctypes.c_uint64, _u64p, _u64p, ctypes.c_size_t,
+                                          ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_primes_up_to.argtypes = [vp, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.bnx_sieve_radicals.argtypes = [
             vp, ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int, _u64p,
@@ -231,6 +233,17 @@ class Context:
         ms = (ctypes.c_float * 4)()
         check(load().bnx_ctx_kernel_timing(self.handle, ms, 4))
         return dict(zip(("count_scan", "screen", "exact", "tail"), (float(v) for v in ms)))
+
+    def class_table(self, max_x: int) -> tuple[np.ndarray, np.ndarray]:
+        """(b, m | r << 40) of the heavy generator's surplus classes for bound max_x, in device order."""
+        count = ctypes.c_size_t(0)
+        with self.lock:
+            check(load().bnx_ctx_class_table(self.handle, max_x, None, None, 0, ctypes.byref(count)))
+            b = np.empty(max(1, count.value), np.uint64)
+            mr = np.empty(max(1, count.value), np.uint64)
+            check(load().bnx_ctx_class_table(self.handle, max_x, b.ctypes.data_as(_u64p), mr.ctypes.data_as(_u64p),
+                                             b.size, ctypes.byref(count)))
+        return b[: count.value], mr[: count.value]
 
     # -- primes ---------------------------------------------------------------------
     def primes_up_to(self, limit: int) -> np.ndarray:

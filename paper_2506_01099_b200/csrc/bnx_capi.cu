@@ -7,11 +7,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/benelux_b200.h"
@@ -40,23 +43,28 @@ int fail(int code, const std::string& msg) {
         if (r_ != BNX_OK) return r_; \
     } while (0)
 
+// Device buffers come from the device's stream-ordered memory pool (cudaMallocAsync on the
+// active context's stream; the pool keeps freed memory, so a new context or a grown buffer
+// does not map fresh pages or synchronise the device the way cudaMalloc / cudaFree do).
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t cap = 0;
     int ensure(size_t n) {
         if (n <= cap && p) return BNX_OK;
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, g_alloc_stream);
         p = nullptr;
         cap = 0;
         size_t want = std::max<size_t>(n, 1);
-        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
-        if (e != cudaSuccess) return fail(BNX_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        cudaError_t e = cudaMallocAsync((void**)&p, want * sizeof(T), g_alloc_stream);
+        if (e != cudaSuccess) return fail(BNX_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
         cap = want;
         return BNX_OK;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, g_alloc_stream);
         p = nullptr;
         cap = 0;
     }
@@ -116,7 +124,26 @@ struct HeavyTab {
     int ntasks = 0, tasks_np2 = -1, tasks_kc = 0;
     DBuf<unsigned char> scan_temp;
     size_t scan_bytes = 0;
+    // device build of the class table (bnx_classes.cu): factor table, per-v counts and
+    // offsets, unsorted classes, sort keys and permutations, cub scratch
+    DBuf<uint32_t> ftab;
+    DBuf<uint64_t> vcnt, voff, keys, key_tmp;
+    DBuf<BnxHeavyEnt> ent_tmp;
+    DBuf<uint32_t> perm, perm_tmp;
+    DBuf<unsigned char> cls_scratch;
+    void release_build() {
+        ftab.release();
+        vcnt.release();
+        voff.release();
+        keys.release();
+        key_tmp.release();
+        ent_tmp.release();
+        perm.release();
+        perm_tmp.release();
+        cls_scratch.release();
+    }
     void release() {
+        release_build();
         ent.release();
         kinfo.release();
         cnt.release();
@@ -141,8 +168,6 @@ struct bnx_ctx {
     bool own_stream = false;
     cudaStream_t aux = nullptr;  // second stream: k_tail_heavy beside k_tail (heavy engine)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    cudaEvent_t h2d_ev = nullptr;   // an unchanged prime list's copy, on `aux` beside the search
-    bool overlap_h2d = false, h2d_pending = false;
     // the heavy engine's search as a CUDA graph, re-captured whenever its parameters change
     bool use_graphs = true;
     cudaGraph_t graph = nullptr, graph2 = nullptr;
@@ -166,6 +191,8 @@ struct bnx_ctx {
     Tables screen_tab, sieve_tab, td_tab;
     HeavyTab heavy_tab;
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
+    bool trace = false;         // BNX_TRACE=1 (see Trace)
+    bool host_classes = false;  // BNX_HOST_CLASSES=1: the class table by the host DFS (tests)
     uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
     int heavy_grid = 0;       // tuning only (BNX_HEAVY_GRID, CTAs per SM); 0 = default
     int heavy_runs = -1;      // tuning only (BNX_HEAVY_RUNS, fetched screen runs per CTA); -1 = default
@@ -231,9 +258,50 @@ struct bnx_table {
 
 namespace {
 
+// Once per device and process: load every search-path kernel (CUDA loads kernels lazily at
+// their first launch, which would otherwise fall inside the first search of a context).
+cudaError_t preload_device(int device, cudaStream_t st) {
+    static std::mutex mu;
+    static std::vector<bool> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)done.size() <= device) done.resize(device + 1, false);
+    if (done[device]) return cudaSuccess;
+    cudaError_t e = heavy_configure();
+    if (e == cudaSuccess) e = kernels_preload();
+    if (e == cudaSuccess) e = classes_preload(st);
+    if (e == cudaSuccess) e = heavy_preload_cub(st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) done[device] = true;
+    return e;
+}
+
+// BNX_TRACE=1: host wall time of each setup phase (stream synchronised), to stderr.
+struct Trace {
+    bnx_ctx* c;
+    std::chrono::steady_clock::time_point t;
+    explicit Trace(bnx_ctx* ctx);
+    void mark(const char* what);
+};
+
 int activate(bnx_ctx* c) {
     CK(cudaSetDevice(c->device));
+    g_alloc_stream = c->stream;
     return BNX_OK;
+}
+
+Trace::Trace(bnx_ctx* ctx) : c(ctx) {
+    if (c->trace) {
+        cudaStreamSynchronize(c->stream);
+        t = std::chrono::steady_clock::now();
+    }
+}
+
+void Trace::mark(const char* what) {
+    if (!c->trace) return;
+    cudaStreamSynchronize(c->stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bnx] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
 }
 
 // Device Eratosthenes up to `limit` (< 2^32): base primes by one block, then a segmented
@@ -292,22 +360,14 @@ int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
     size_t k = (size_t)(std::upper_bound(primes, primes + np, need) - primes);
     TRY(c->stage64.ensure(k));
     TRY(c->primes.ensure(k));
-    // The copy always happens (the caller's buffer is the input of every call); the 32-bit
-    // device list and the tables derived from it are rebuilt only if the list changed.
+    // The list is compared with the host copy of the one the device tables were built from;
+    // only a changed list is copied to the device (and the tables rebuilt).
     const bool same = c->gen > 0 && c->h_primes64.size() == k && c->primes_limit == need &&
                       (k == 0 || std::memcmp(c->h_primes64.data(), primes, sizeof(uint64_t) * k) == 0);
-    if (k && same && c->overlap_h2d) {
-        // nothing on the device reads this copy (the tables it would feed are current): it
-        // runs on the second stream beside the search and is joined before the call returns
-        CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->aux));
-        CK(cudaEventRecord(c->h2d_ev, c->aux));
-        c->h2d_pending = true;
-    } else if (k) {
+    if (k && !same) {
         CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->stream));
-        if (!same) {
-            launch_narrow(c->stage64.p, k, c->primes.p, c->stream);
-            CK(cudaGetLastError());
-        }
+        launch_narrow(c->stage64.p, k, c->primes.p, c->stream);
+        CK(cudaGetLastError());
     }
     if (!same) {
         c->h_primes.resize(k);
@@ -435,60 +495,101 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
 // The surplus classes: every powerful b = prod p^(e+1) <= max_x (DFS over the primes up to
 // sqrt(max_x)) with sigma = prod p^e = m r, r = prod p; and kinfo[k] for k <= sqrt(max_x / 2)
 // (the largest k any class can use: k^2 <= 2m * max_x / (m r^2) <= max_x / 2 for r >= 2).
+int build_heavy_host(bnx_ctx* c, uint64_t max_x);
+
+// The surplus-class table on the device (bnx_classes.cu): one host sync, to size the table.
 int build_heavy(bnx_ctx* c, uint64_t max_x) {
     HeavyTab& h = c->heavy_tab;
     // a table for a larger bound serves (its extra classes count zero items), unless it is so
     // much larger that the per-search class pass would dominate: then rebuild for this bound
     if (h.gen == c->gen && h.max_x >= max_x && h.max_x / 16 <= max_x) return BNX_OK;
+    if (c->host_classes) return build_heavy_host(c, max_x);
     const std::vector<uint32_t>& P = c->h_primes;
     const uint64_t root = isqrt_u64(max_x);
-    if (P.empty() || (P.back() < root && c->primes_limit < root))
+    if (c->primes_limit < root && (P.empty() || P.back() < root))
+        return fail(BNX_ERR_PRIMES_UNCOVERED, "prime table does not cover sqrt(bound)");
+    const uint64_t K = isqrt_u64(max_x / 2) + 3;  // kinfo entries (see build_heavy_host)
+    const uint64_t Ltab = std::max<uint64_t>(root, K);
+    auto upto = [&](uint64_t v) {
+        return (uint64_t)(std::upper_bound(P.begin(), P.end(), (uint32_t)std::min<uint64_t>(v, 0xFFFFFFFFull)) - P.begin());
+    };
+    const ClassPlan pl = class_plan(max_x, upto(root));
+    if (!pl.ok) return fail(BNX_ERR_RANGE, "class table key too long");
+    Trace tr(c);
+    TRY(h.ftab.ensure(Ltab + 1));
+    TRY(h.vcnt.ensure(pl.V + 2));
+    TRY(h.voff.ensure(pl.V + 2));
+    size_t sb = class_scratch_bytes(pl, 0);
+    TRY(h.cls_scratch.ensure(sb));
+    CK(class_count(pl, Ltab, c->primes.p, upto(Ltab), h.ftab.p, h.vcnt.p, h.voff.p, h.cls_scratch.p, h.cls_scratch.cap,
+                   c->stream));
+    uint64_t total = 0;
+    CK(cudaMemcpyAsync(&total, h.voff.p + pl.V + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    tr.mark("classes: factor table + count");
+    if (total == 0 || total > 0xFFFFFFFFull) return fail(BNX_ERR_CUDA, "class table size out of range");
+    sb = class_scratch_bytes(pl, total);
+    TRY(h.cls_scratch.ensure(sb));
+    TRY(h.ent_tmp.ensure(total));
+    TRY(h.ent.ensure(total));
+    TRY(h.keys.ensure(total * pl.nwords));
+    TRY(h.key_tmp.ensure(total));
+    TRY(h.perm.ensure(total));
+    TRY(h.perm_tmp.ensure(total));
+    TRY(h.kinfo.ensure(K));
+    tr.mark("classes: allocate");
+    CK(class_build(pl, total, c->primes.p, h.ftab.p, h.voff.p, h.ent_tmp.p, h.ent.p, h.keys.p, h.key_tmp.p, h.perm.p,
+                   h.perm_tmp.p, h.cls_scratch.p, h.cls_scratch.cap, h.kinfo.p, K, c->stream));
+    tr.mark("classes: build + sort");
+    TRY(h.cnt.ensure(total));
+    TRY(h.incl.ensure(total));
+    TRY(h.klo.ensure(total));
+    TRY(h.kcnt.ensure(total));
+    h.scan_bytes = heavy_scan_temp_bytes(total);
+    TRY(h.scan_temp.ensure(h.scan_bytes));
+    tr.mark("classes: search buffers");
+    h.nent = total;
+    h.nkinfo = K;
+    h.max_x = max_x;
+    h.gen = c->gen;
+    return BNX_OK;
+}
+
+// The same table by a depth-first search on the host (BNX_HOST_CLASSES=1; tests compare the
+// two): every powerful b = prod p^(e+1) <= max_x (DFS over the primes up to sqrt(max_x)) with
+// sigma = prod p^e = m r, r = prod p; and kinfo[k] for k <= sqrt(max_x / 2) (the largest k
+// any class can use: k^2 <= 2m * max_x / (m r^2) <= max_x / 2 for r >= 2).
+int build_heavy_host(bnx_ctx* c, uint64_t max_x) {
+    HeavyTab& h = c->heavy_tab;
+    const std::vector<uint32_t>& P = c->h_primes;
+    const uint64_t root = isqrt_u64(max_x);
+    if (root >= 2 && (P.empty() || (P.back() < root && c->primes_limit < root)))
         return fail(BNX_ERR_PRIMES_UNCOVERED, "prime table does not cover sqrt(bound)");
     std::vector<BnxHeavyEnt> ents;
-    std::vector<uint64_t> vkey;  // (experiment, BNX_HEAVY_ORDER=2) v of b = u^2 v^3, v squarefree
     ents.reserve((size_t)(2.5 * std::sqrt((double)max_x)) + 64);
-    struct Node { uint64_t b, sigma, r; uint32_t rmask, rbig, rbig_min; size_t next; uint64_t v; };
+    struct Node { uint64_t b, sigma, r; uint32_t rmask, rbig, rbig_min; size_t next; };
     std::vector<Node> stack;
-    stack.push_back(Node{1, 1, 1, 0, 1, 0, 0, 1});
+    stack.push_back(Node{1, 1, 1, 0, 1, 0, 0});
     while (!stack.empty()) {
         const Node f = stack.back();
         stack.pop_back();
         ents.push_back(BnxHeavyEnt{f.b, f.sigma / f.r, (uint32_t)f.r, f.rmask, f.rbig, f.rbig_min});
-        vkey.push_back(f.v);
         for (size_t i = f.next; i < P.size(); ++i) {
             const uint64_t p = P[i];
             if (p > root || f.b > max_x / (p * p)) break;
-            Node ch{f.b * p * p, f.sigma * p, f.r * p, f.rmask, f.rbig, f.rbig_min, i + 1, f.v};
+            Node ch{f.b * p * p, f.sigma * p, f.r * p, f.rmask, f.rbig, f.rbig_min, i + 1};
             if (i < 31) ch.rmask |= 1u << i;
             else {
                 ch.rbig = (uint32_t)(f.rbig * p);
                 if (!ch.rbig_min) ch.rbig_min = (uint32_t)p;
             }
-            bool odd = false;
             for (;;) {
                 stack.push_back(ch);
                 if (ch.b > max_x / p) break;
                 ch.b *= p;
                 ch.sigma *= p;
-                odd = !odd;
-                ch.v = odd ? f.v * p : f.v;
             }
         }
-    }
-    if (const char* env = std::getenv("BNX_HEAVY_ORDER")) {  // class-order experiment
-        const int order = std::atoi(env);
-        std::vector<size_t> idx(ents.size());
-        for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
-        auto ukey = [&](size_t i) { return (uint64_t)std::llround(std::sqrt((double)(ents[i].b / (vkey[i] * vkey[i] * vkey[i])))); };
-        if (order == 1) std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return ents[a].b < ents[b].b; });
-        if (order == 2)
-            std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
-                return vkey[a] != vkey[b] ? vkey[a] < vkey[b] : ukey(a) < ukey(b);
-            });
-        if (order == 3) std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return ents[a].b > ents[b].b; });
-        std::vector<BnxHeavyEnt> sorted(ents.size());
-        for (size_t i = 0; i < idx.size(); ++i) sorted[i] = ents[idx[i]];
-        ents.swap(sorted);
     }
     // (kept in DFS order: classes of one prime structure stay together, which measured ~10%
     // faster at 2^32 than sorting by sigma, and the host sort cost 0.35 s at 2^40, 7 s at 2^48;
@@ -533,14 +634,8 @@ int ensure_pairs(bnx_ctx* c, size_t rows) {
 
 int ensure_work(bnx_ctx* c) {
     if (!c->surv.p) TRY(c->surv.ensure(1 << 20));
-    if (!c->heavy.p) TRY(c->heavy.ensure(64));
+    if (!c->heavy.p) TRY(c->heavy.ensure(1 << 16));  // (k_tail_heavy's list: a few hundred below 1.4e12)
     if (!c->pairs_p) TRY(ensure_pairs(c, 1 << 14));
-    if (!c->h_io) {
-        CK(cudaMallocHost(&c->h_io, IO_PAIRS + sizeof(bnx_pair_t) * PAIR_PREFIX));
-        c->h_sctr = reinterpret_cast<unsigned long long*>(c->h_io + IO_CTR);
-        c->h_sflags = reinterpret_cast<int*>(c->h_io + IO_FLAGS);
-        c->h_pairs = reinterpret_cast<bnx_pair_t*>(c->h_io + IO_PAIRS);
-    }
     return BNX_OK;
 }
 
@@ -564,10 +659,15 @@ uint64_t iroot4_u64(uint64_t x) {
 // Heavy engine: k_heavy_count, scan, k_heavy_screen, k_heavy_exact, then the tail on the
 // exact candidates.
 int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) {
+    Trace tr(c);
     HeavyTab& h = c->heavy_tab;
     Tables& t = c->screen_tab;  // pdiv: odd primes <= sqrt(bound)
     TRY(ensure_work(c));
-    if (!c->q1.p) TRY(c->q1.ensure(1 << 20));
+    {  // screen survivors grow like sqrt(bound) (88,139 below 2^32, 1.45M below 1.4e12): sized
+        // up front so that a first search does not overflow, grow and run again
+        const double est = 1.3 * 88139.0 * std::sqrt((double)(n_last + 1) / 4294967296.0) + 65536.0;
+        TRY(c->q1.ensure(std::max<size_t>(c->q1.cap, (size_t)std::min(est, 1e9))));
+    }
     if (!c->cand.p) TRY(c->cand.ensure(1 << 16));
     const uint64_t y_max = n_last + 2;
     const uint64_t p2 = iroot4_u64(y_max), p3 = icbrt_u64(y_max);
@@ -600,13 +700,12 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         for (uint64_t j = 0; j < np2; ++j) {
             const uint32_t p = c->h_primes[j + (c->h_primes[0] == 2 ? 1 : 0)];
             ioff.push_back((uint32_t)itab.size());
-            itab.push_back(0);
-            for (uint32_t v = 1; v < p; ++v) {  // v^-1 = v^(p-2) mod p
-                uint64_t r = 1, base = v, e = p - 2;
-                for (; e; e >>= 1, base = base * base % p)
-                    if (e & 1) r = r * base % p;
-                itab.push_back((uint16_t)r);
-            }
+            const size_t o = itab.size();
+            itab.resize(o + p);
+            itab[o] = 0;
+            if (p > 1) itab[o + 1] = 1;
+            for (uint32_t v = 2; v < p; ++v)  // v^-1 = -(p / v) (p mod v)^-1 (mod p)
+                itab[o + v] = (uint16_t)((uint64_t)(p - p / v) * itab[o + p % v] % p);
             const uint32_t hits = (uint32_t)((kc + p - 1) / p);
             const uint32_t R = std::max<uint32_t>(1, (hits + HEAVY_TASK_HITS - 1) / HEAVY_TASK_HITS);
             for (uint32_t side = 0; side < 2; ++side)
@@ -624,6 +723,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         h.tasks_np2 = (int)np2;
         h.tasks_kc = kc;
     }
+    tr.mark("enqueue: sieve tasks");
     HeavyArgs ha;
     std::memset(&ha, 0, sizeof(ha));  // (the graph key compares bytes, padding included)
     ha.kcnt = h.kcnt.p;
@@ -755,6 +855,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
                 TRY(capture(record_tail, &c->graph2, &c->graph_exec2));
             }
             c->graph_key = key;
+            tr.mark("enqueue: graph capture");
         }
         if (single) {
             CK(cudaGraphLaunch(c->graph_exec, c->stream));
@@ -851,12 +952,15 @@ int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint6
     if (c->engine != 0 && max_x >= (1ull << 42))
         return fail(BNX_ERR_RANGE, "search bound must be below 2^42 with the byte-screen engine");
     const uint64_t need = isqrt_u64(max_x);
+    Trace tr(c);
     TRY(ensure_primes(c, primes, np, plimit, need));
+    tr.mark("prepare: primes");
     TRY(build_tables(c, c->screen_tab, max_x, 0, (uint32_t)screen_variant(c->screen_v).tile,
                      screen_variant(c->screen_v).threads / 32));
-
+    tr.mark("prepare: progression tables");
     if (c->screen_tab.nsmall > (uint32_t)SCREEN_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     if (c->engine == 0) TRY(build_heavy(c, max_x));
+    tr.mark("prepare: class table");
     return BNX_OK;
 }
 
@@ -917,17 +1021,13 @@ int search_rows(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds, c
     if (n_first < 1 || n_last < n_first) return fail(BNX_ERR_INVALID, "empty search domain");
     if ((kinds & 3u) == 0) return fail(BNX_ERR_INVALID, "kinds_mask selects no kind");
     TRY(activate(c));
-    c->overlap_h2d = true;
-    const int rc = prepare(c, n_last + 1, primes, np, plimit);
-    c->overlap_h2d = false;
-    int rc2 = rc == BNX_OK ? enqueue(c, n_first, n_last, kinds & 3u) : rc;
-    if (c->h2d_pending) {  // the caller's buffer is read before the call returns
-        c->h2d_pending = false;
-        CK(cudaStreamWaitEvent(c->stream, c->h2d_ev, 0));
-        if (rc2 != BNX_OK) CK(cudaStreamSynchronize(c->aux));
-    }
-    TRY(rc2);
-    return collect(c, rows);
+    TRY(prepare(c, n_last + 1, primes, np, plimit));
+    Trace tr(c);
+    TRY(enqueue(c, n_first, n_last, kinds & 3u));
+    tr.mark("search: enqueue (+ capture)");
+    TRY(collect(c, rows));
+    tr.mark("search: device + collect");
+    return BNX_OK;
 }
 
 }  // namespace
@@ -957,15 +1057,27 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
+    g_alloc_stream = c->stream;
+    {  // the pool keeps what contexts free (DBuf); load this library's kernels once per device
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        CK(preload_device(device, c->stream));
+        CK(cudaMallocHost(&c->h_io, IO_PAIRS + sizeof(bnx_pair_t) * PAIR_PREFIX));
+        c->h_sctr = reinterpret_cast<unsigned long long*>(c->h_io + IO_CTR);
+        c->h_sflags = reinterpret_cast<int*>(c->h_io + IO_FLAGS);
+        c->h_pairs = reinterpret_cast<bnx_pair_t*>(c->h_io + IO_PAIRS);
+    }
     CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&c->h2d_ev, cudaEventDisableTiming));
-    CK(heavy_configure());
     if (const char* env = std::getenv("BNX_GRAPHS")) c->use_graphs = std::atoi(env) != 0;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
+    if (const char* env = std::getenv("BNX_TRACE")) c->trace = std::atoi(env) != 0;
+    if (const char* env = std::getenv("BNX_HOST_CLASSES")) c->host_classes = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_HEAVY_KMIN")) c->heavy_kmin = std::strtoull(env, nullptr, 10);
     if (const char* env = std::getenv("BNX_HEAVY_GRID")) c->heavy_grid = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_RUNS")) c->heavy_runs = std::max(0, std::atoi(env));
@@ -1001,6 +1113,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
 int bnx_ctx_destroy(bnx_ctx_t* c) {
     if (!c) return BNX_OK;
     cudaSetDevice(c->device);
+    g_alloc_stream = c->stream;
     if (c->stream) cudaStreamSynchronize(c->stream);
     c->primes.release();
     c->stage64.release();
@@ -1023,9 +1136,11 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
         if (e) cudaEventDestroy(e);
     for (auto& e : c->kev)
         if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamSynchronize(c->stream);  // (the stream-ordered frees above)
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->h_io) cudaFreeHost(c->h_io);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    g_alloc_stream = nullptr;
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->graph_exec2) cudaGraphExecDestroy(c->graph_exec2);
     if (c->graph) cudaGraphDestroy(c->graph);
@@ -1033,7 +1148,6 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
-    if (c->h2d_ev) cudaEventDestroy(c->h2d_ev);
     delete c;
     return BNX_OK;
 }
@@ -1041,10 +1155,8 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
 int bnx_ctx_set_stream(bnx_ctx_t* c, void* stream) {
     if (!c) return fail(BNX_ERR_INVALID, "null context");
     TRY(activate(c));
-    if (c->own_stream && c->stream) {
-        cudaStreamSynchronize(c->stream);
-        cudaStreamDestroy(c->stream);
-    }
+    cudaStreamSynchronize(c->stream);  // (buffers allocated on it are freed on the new one later)
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (stream) {
         c->stream = (cudaStream_t)stream;
         c->own_stream = false;
@@ -1052,6 +1164,7 @@ int bnx_ctx_set_stream(bnx_ctx_t* c, void* stream) {
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
+    g_alloc_stream = c->stream;
     return BNX_OK;
 }
 
@@ -1072,6 +1185,24 @@ int bnx_ctx_set_timing(bnx_ctx_t* c, int enabled) {
         for (auto& e : c->kev)
             if (!e) CK(cudaEventCreate(&e));
     c->timing = enabled;
+    return BNX_OK;
+}
+
+int bnx_ctx_class_table(bnx_ctx_t* c, uint64_t max_x, uint64_t* b_out, uint64_t* m_out, size_t cap, size_t* count) {
+    if (!c || !count) return fail(BNX_ERR_INVALID, "null argument");
+    if (c->engine != 0) return fail(BNX_ERR_INVALID, "the class table belongs to the heavy engine");
+    TRY(activate(c));
+    TRY(prepare(c, max_x, nullptr, 0, 0));
+    const HeavyTab& h = c->heavy_tab;
+    *count = h.nent;
+    if (h.nent > cap) return fail(BNX_BUFFER_FULL, "class buffer too small");
+    std::vector<BnxHeavyEnt> e(h.nent);
+    CK(cudaMemcpyAsync(e.data(), h.ent.p, sizeof(BnxHeavyEnt) * h.nent, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < e.size(); ++i) {
+        if (b_out) b_out[i] = e[i].b;
+        if (m_out) m_out[i] = e[i].m | (uint64_t)e[i].r << 40;  // (m < 2^24 up to 2^48)
+    }
     return BNX_OK;
 }
 
@@ -1296,11 +1427,23 @@ int bnx_search_multi(const int* devices, int ndev, uint64_t limit, uint32_t kind
             g_multi[i] = nullptr;
         }
         if (!g_multi[i]) TRY(bnx_ctx_create(devices[i], &g_multi[i]));
-        bnx_ctx* c = g_multi[i];
-        TRY(activate(c));
-        c->shard = (uint32_t)i;
-        c->nshards = (uint32_t)ndev;
-        TRY(prepare(c, limit, primes, nprimes, primes_limit));
+        g_multi[i]->shard = (uint32_t)i;
+        g_multi[i]->nshards = (uint32_t)ndev;
+    }
+    {  // the contexts' tables are built concurrently, one host thread per context
+        std::vector<int> rc(ndev, BNX_OK);
+        std::vector<std::string> err(ndev);
+        std::vector<std::thread> th;
+        for (int i = 0; i < ndev; ++i)
+            th.emplace_back([&, i] {
+                bnx_ctx* c = g_multi[i];
+                rc[i] = activate(c);
+                if (rc[i] == BNX_OK) rc[i] = prepare(c, limit, primes, nprimes, primes_limit);
+                if (rc[i] != BNX_OK) err[i] = g_err;
+            });
+        for (auto& t : th) t.join();
+        for (int i = 0; i < ndev; ++i)
+            if (rc[i] != BNX_OK) return fail(rc[i], err[i]);
     }
     for (int i = 0; i < ndev; ++i) {
         TRY(activate(g_multi[i]));
@@ -1402,6 +1545,7 @@ int bnx_table_create(bnx_ctx_t* c, uint64_t table_size, bnx_table_t** out) {
 int bnx_table_destroy(bnx_table_t* tb) {
     if (!tb) return BNX_OK;
     cudaSetDevice(tb->ctx->device);
+    g_alloc_stream = tb->ctx->stream;
     cudaStreamSynchronize(tb->ctx->stream);
     tb->slots.release(); tb->rad_of.release(); tb->rad_next.release();
     tb->probe_of.release(); tb->probe_next.release(); tb->rows.release(); tb->cnt.release(); tb->status.release();

@@ -792,6 +792,25 @@ cudaError_t heavy_configure() {
         e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_heavy_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncAttributes at;  // (the attribute calls above load those three; see kernels_preload)
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, k_heavy_count);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, k_pdiv32);
+    return e;
+}
+
+// The cub scan this file launches, run once on two elements (loads its kernels).
+cudaError_t heavy_preload_cub(cudaStream_t st) {
+    uint64_t* d = nullptr;
+    void* tmp = nullptr;
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, d, d, (int64_t)2);
+    cudaError_t e = cudaMallocAsync((void**)&d, 4 * sizeof(uint64_t) + bytes + 256, st);
+    if (e != cudaSuccess) return e;
+    tmp = (void*)(d + 4);
+    cudaMemsetAsync(d, 0, 2 * sizeof(uint64_t), st);
+    cub::DeviceScan::InclusiveSum(tmp, bytes, d, d + 2, (int64_t)2, st);
+    e = cudaGetLastError();
+    cudaFreeAsync(d, st);
     return e;
 }
 

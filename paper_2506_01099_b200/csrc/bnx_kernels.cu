@@ -486,22 +486,24 @@ __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
     }
 }
 
-// Heavy candidates: blockIdx.y picks the candidate, the warps of the x-blocks split its members
-// into chunks of 32.
+// Heavy candidates: blockIdx.y picks the candidate (strided over the list), the warps of the
+// x-blocks split its members into chunks of 32.
 __global__ void __launch_bounds__(256) k_tail_heavy(TailArgs a) {
     const uint64_t nh = min((uint64_t)a.ctr[CTR_HEAVY], a.heavy_cap);
-    if (blockIdx.y >= nh) return;
-    const BnxCand h = a.heavy[blockIdx.y];
-    TailCand c;
-    c.n = h.n; c.r0 = h.r0; c.r1 = h.r1; c.R = h.r0 * h.r1;
-    c.s0 = h.n / h.r0; c.s1 = (h.n + 1) / h.r1;
-    c.t1 = (a.kinds & 1u) ? (h.n - 1) / c.R : 0;
-    c.t0 = (h.n + 1) / c.R + 1;
-    const uint64_t t2 = (2 * h.n) / c.R;
-    const uint64_t total = c.t1 + (((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0);
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t chunk = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); chunk * 32 < total; chunk += nwarps)
-        tail_members(a, c, chunk * 32, min(total, chunk * 32 + 32));
+    for (uint64_t y = blockIdx.y; y < nh; y += gridDim.y) {
+        const BnxCand h = a.heavy[y];
+        TailCand c;
+        c.n = h.n; c.r0 = h.r0; c.r1 = h.r1; c.R = h.r0 * h.r1;
+        c.s0 = h.n / h.r0; c.s1 = (h.n + 1) / h.r1;
+        c.t1 = (a.kinds & 1u) ? (h.n - 1) / c.R : 0;
+        c.t0 = (h.n + 1) / c.R + 1;
+        const uint64_t t2 = (2 * h.n) / c.R;
+        const uint64_t total = c.t1 + (((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0);
+        const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+        for (uint64_t chunk = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); chunk * 32 < total;
+             chunk += nwarps)
+            tail_members(a, c, chunk * 32, min(total, chunk * 32 + 32));
+    }
 }
 
 // ------------------------------------------------------------------------------------
@@ -813,9 +815,10 @@ static const ScreenVariant kScreenVariants[] = {
 };
 int screen_variant_count() { return (int)(sizeof(kScreenVariants) / sizeof(kScreenVariants[0])); }
 const ScreenVariant& screen_variant(int i) { return kScreenVariants[i]; }
+constexpr unsigned TAIL_HEAVY_Y = 256;  // k_tail_heavy grid rows (candidates strided over them)
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st) {
     k_tail<<<grid, 256, 0, st>>>(a);
-    k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);
+    k_tail_heavy<<<dim3(8, (unsigned)std::min<uint64_t>(a.heavy_cap, TAIL_HEAVY_Y)), 256, 0, st>>>(a);
 }
 void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st, bool pdl) {
     cudaLaunchConfig_t cfg = {};
@@ -830,7 +833,7 @@ void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st, bool pdl) {
     cudaLaunchKernelEx(&cfg, k_tail, a);
 }
 void launch_tail_heavy(const TailArgs& a, cudaStream_t st) {
-    k_tail_heavy<<<dim3(8, (unsigned)a.heavy_cap), 256, 0, st>>>(a);
+    k_tail_heavy<<<dim3(8, (unsigned)std::min<uint64_t>(a.heavy_cap, TAIL_HEAVY_Y)), 256, 0, st>>>(a);
 }
 
 void launch_base_primes(uint32_t ls, uint32_t* out, uint32_t* count, cudaStream_t st) {
@@ -867,6 +870,20 @@ void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st) { k_table
 void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out,
                            int grid, cudaStream_t st) {
     k_trial_division<<<grid, 256, 0, st>>>(start, length, pd, npd, out);
+}
+
+// Load the search-path kernels of this file now (CUDA loads a kernel lazily at its first
+// launch, which would otherwise land inside a caller's first search).
+cudaError_t kernels_preload() {
+    const void* fns[] = {(const void*)k_base_primes, (const void*)k_prime_seg, (const void*)k_scan_counts,
+                         (const void*)k_narrow_primes, (const void*)k_build_tables, (const void*)k_tail,
+                         (const void*)k_tail_heavy, kSieveVariants[0].fn, kScreenVariants[0].fn};
+    for (const void* f : fns) {
+        cudaFuncAttributes at;
+        const cudaError_t e = cudaFuncGetAttributes(&at, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace bnx

@@ -120,6 +120,25 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
                   cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join,
                   const cudaEvent_t* kev = nullptr);  // kev[0..3]: per-kernel timing (count, screen, exact)
 
+// The surplus-class table built on the device (bnx_classes.cu).
+struct ClassPlan {
+    uint64_t X, L, V;  // bound, isqrt(X) (factor table), icbrt(X) (the v of b = u^2 v^3)
+    int D, bits, dpw, nwords;  // sort key: D codes of `bits` bits, dpw per 64-bit word
+    bool ok;
+};
+ClassPlan class_plan(uint64_t X, uint64_t nprimes_root);
+cudaError_t classes_preload(cudaStream_t st);
+cudaError_t kernels_preload();
+cudaError_t heavy_preload_cub(cudaStream_t st);
+size_t class_scratch_bytes(const ClassPlan& pl, uint64_t total);
+// tab: Ltab + 1 entries (Ltab >= pl.L; np_tab = primes <= Ltab in the list); cnt, offs: V + 2
+cudaError_t class_count(const ClassPlan& pl, uint64_t Ltab, const uint32_t* primes, uint64_t np_tab, uint32_t* tab,
+                        uint64_t* cnt, uint64_t* offs, void* scratch, size_t scratch_bytes, cudaStream_t st);
+cudaError_t class_build(const ClassPlan& pl, uint64_t total, const uint32_t* primes, const uint32_t* tab,
+                        const uint64_t* offs, BnxHeavyEnt* ent_tmp, BnxHeavyEnt* ent, uint64_t* keys,
+                        uint64_t* key_tmp, uint32_t* perm, uint32_t* perm_tmp, void* scratch, size_t scratch_bytes,
+                        uint32_t* kinfo, uint64_t K, cudaStream_t st);
+
 struct SieveArgs {
     uint64_t start, length;
     const BnxProg* small;
