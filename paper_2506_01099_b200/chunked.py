@@ -124,6 +124,15 @@ def search_chunk(
     return pairs_from_rows(search_rows(dom[0], dom[1], primes=primes, device=device))
 
 
+def _prepare_run(limit: int, primes: PrimeList | None, device: int | None) -> None:
+    """Build the device tables once for the run's final bound; the batch searches (rising
+    bounds) then reuse them instead of rebuilding per batch."""
+    from . import _native
+
+    _native.context(device).prepare(limit, None if primes is None else primes.primes,
+                                    0 if primes is None else primes.limit)
+
+
 def run_full_chunked(
     limit: int,
     chunk_size: int = DEFAULT_CHUNK_SIZE,
@@ -146,6 +155,8 @@ def run_full_chunked(
         if not primes.covers(need):
             raise ValueError(f"prime list covers {primes.limit} but interval endpoint needs {need}")
     per_batch = max(1, BATCH_INTEGERS // (chunk_size - 1))
+    if resume_from < total:
+        _prepare_run(limit, primes, device)
     index = resume_from
     while index < total:
         stop = min(total, index + per_batch)

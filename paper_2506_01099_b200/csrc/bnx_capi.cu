@@ -362,7 +362,10 @@ int upload_primes(bnx_ctx* c, const uint64_t* primes, size_t np, uint64_t primes
     TRY(c->primes.ensure(k));
     // The list is compared with the host copy of the one the device tables were built from;
     // only a changed list is copied to the device (and the tables rebuilt).
-    const bool same = c->gen > 0 && c->h_primes64.size() == k && c->primes_limit == need &&
+    // (a list already on the device that extends this one serves too: a streaming run
+    // prepares for its final bound once, then searches batches with smaller bounds)
+    const bool same = c->gen > 0 && c->h_primes64.size() >= k && c->primes_limit >= need &&
+                      (c->h_primes64.size() == k || c->h_primes64[k] > need) &&
                       (k == 0 || std::memcmp(c->h_primes64.data(), primes, sizeof(uint64_t) * k) == 0);
     if (k && !same) {
         CK(cudaMemcpyAsync(c->stage64.p, primes, sizeof(uint64_t) * k, cudaMemcpyHostToDevice, c->stream));
@@ -503,6 +506,13 @@ int build_heavy(bnx_ctx* c, uint64_t max_x) {
     // a table for a larger bound serves (its extra classes count zero items), unless it is so
     // much larger that the per-search class pass would dominate: then rebuild for this bound
     if (h.gen == c->gen && h.max_x >= max_x && h.max_x / 16 <= max_x) return BNX_OK;
+    if (h.gen == c->gen && h.max_x && h.max_x < max_x) {
+        // growing (a streaming run's batches come in with rising bounds): build for twice the
+        // old bound at least, so a run to S rebuilds O(log S) times -- if the primes cover it
+        const uint64_t grown = std::min<uint64_t>(std::max<uint64_t>(max_x, 2 * h.max_x), 1ull << 48);
+        if (c->primes_limit >= isqrt_u64(grown) || (!c->h_primes.empty() && c->h_primes.back() >= isqrt_u64(grown)))
+            max_x = grown;
+    }
     if (c->host_classes) return build_heavy_host(c, max_x);
     const std::vector<uint32_t>& P = c->h_primes;
     const uint64_t root = isqrt_u64(max_x);
@@ -541,6 +551,7 @@ int build_heavy(bnx_ctx* c, uint64_t max_x) {
     CK(class_build(pl, total, c->primes.p, h.ftab.p, h.voff.p, h.ent_tmp.p, h.ent.p, h.keys.p, h.key_tmp.p, h.perm.p,
                    h.perm_tmp.p, h.cls_scratch.p, h.cls_scratch.cap, h.kinfo.p, K, c->stream));
     tr.mark("classes: build + sort");
+    h.release_build();  // (stream-ordered: the per-search buffers below reuse the memory)
     TRY(h.cnt.ensure(total));
     TRY(h.incl.ensure(total));
     TRY(h.klo.ensure(total));
@@ -1605,9 +1616,13 @@ int bnx_table_search_chunk(bnx_ctx_t* c, uint64_t index, uint64_t chunk_size, ui
     if (chunk_size < 3) return fail(BNX_ERR_INVALID, "chunk size must be >= 3");
     TRY(activate(c));
     const uint64_t s = chunk_size, count = s - 1;
+    // the slot word keeps the home slot in 32 bits and the offset + 1 in the other 32
+    // (chunked.py:136-138, :157-158): the reference refuses larger tables (ValueError)
+    if (count > 0xFFFFFFFEull || count > (1ull << 30)) return fail(BNX_ERR_INVALID, "chunk too large for 32-bit slots");
     uint64_t v = 4 * count - 1, bits = 0;
     while (v) { ++bits; v >>= 1; }
     const uint64_t tsize = 1ull << bits;  // table_size_for (chunked.py:86-90)
+    if (tsize > (1ull << 32)) return fail(BNX_ERR_INVALID, "table too large for 32-bit home slots");
     bnx_table tb;
     tb.ctx = c;
     tb.size = tsize;

@@ -123,6 +123,8 @@ def search_chunk_table(index: int, chunk_size: int, *, n_limit: int | None = Non
     """chunked.py:307-359 with Algorithm 3 on the device (sorted by (n, m))."""
     if chunk_size < 3:
         raise ValueError("chunk size must be >= 3")
+    if chunk_size - 1 > 1 << 30:  # table_size_for would exceed 2^32 slots (chunked.py:157-158)
+        raise ValueError("chunk size too large for 32-bit table slots")
     ctx = _native.context(device)
     hi = index if j_hi is None else j_hi
     limit = 2**64 - 1 if n_limit is None else n_limit

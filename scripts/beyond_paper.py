@@ -1,6 +1,6 @@
 """Both kinds below S on one B200 with the heavy generator, for S beyond the paper's range
 (1.4e12): every pair found is re-verified on the CPU (exact radicals of m, m+1, n, n+1 by
-trial division) and compared with the known infinite families (families.py); one JSON line
+trial division) and compared with the known infinite families (oracle/theorem1.py); one JSON line
 per bound.
 
     python scripts/beyond_paper.py 2^42 2^43 2^44
@@ -38,12 +38,9 @@ for arg in sys.argv[1:] or ["2^44"]:
         (bp.radical_oracle(m), bp.radical_oracle(m + 1)) ==
         ((bp.radical_oracle(n), bp.radical_oracle(n + 1)) if k == 1 else (bp.radical_oracle(n + 1), bp.radical_oracle(n)))
         for m, n, k in pairs)
-    # the known families (families.py) continued past the completeness bound
-    from paper_2506_01099_b200 import families as fm
-    known = [(m, n, 1) for m, n in (fm.family_first_kind(k) for k in range(2, 32)) if n < S]
-    known += [(m, n, 2) for m, n in (fm.family_second_kind(k) for k in range(0, 32)) if n < S]
-    known += [(p.m, p.n, int(p.kind)) for p in fm.exceptional_pairs() if p.n < S]
-    known.sort()
+    # the known families (oracle/theorem1.py) continued past the completeness bound
+    from oracle import theorem1
+    known = sorted((m, n, k) for k, m, n, _, _ in theorem1.known_rows(S, beyond_bound=True))
     extra = [p for p in pairs if p not in known]
     missing = [p for p in known if p not in pairs]
     print(json.dumps({"S": S, "pairs": len(pairs), "first": sum(k == 1 for *_, k in pairs),

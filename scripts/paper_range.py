@@ -11,7 +11,8 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-import paper_2506_01099_b200 as bp  # noqa: E402
+import paper_2506_01099_b200 as bp
+from oracle import theorem1  # noqa: E402
 
 
 def parse_bound(s: str) -> int:
@@ -33,11 +34,11 @@ def main() -> None:
         t0 = time.perf_counter()
         pairs = bp.find_pairs(S, kinds=None if args.kinds == "both" else args.kinds)
         wall = time.perf_counter() - t0
-        exp = bp.expected_pairs_up_to(S)
+        exp = theorem1.known_rows(S)
         got1 = sorted((p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in pairs if p.kind == bp.Kind.FIRST)
         got2 = sorted((p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in pairs if p.kind == bp.Kind.SECOND)
-        e1 = sorted((p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in exp.first_kind)
-        e2 = sorted((p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in exp.second_kind)
+        e1 = sorted(tuple(r[1:]) for r in exp if r[0] == 1)
+        e2 = sorted(tuple(r[1:]) for r in exp if r[0] == 2)
         ok = (args.kinds in ("both", "first") and got1 == e1 or args.kinds == "second") and \
              (args.kinds in ("both", "second") and got2 == e2 or args.kinds == "first")
         rec = {"S": S, "bound": tok, "wall_s": wall, "int_per_s": (S - 1) / wall, "first": len(got1),

@@ -277,9 +277,10 @@ def test_engines_agree(lo, hi):
 def test_whole_range_to_2p40_is_theorem_1():
     """One device search over [1, 2^40) (both kinds): exactly the 41 pairs of Theorem 1."""
     S = 1 << 40
+    from oracle import theorem1
+
     got = sorted((p.m, p.n) for p in bp.find_pairs(S))
-    exp = bp.expected_pairs_up_to(S)
-    assert got == sorted((p.m, p.n) for p in exp.first_kind + exp.second_kind)
+    assert got == theorem1.known_pairs(S)
     assert len(got) == 41
 
 

@@ -58,12 +58,17 @@ def test_host_helpers_match_reference(golden):
     assert [bp.radical_oracle(n) for n in (1, 75, 1216, 1218)] == [1, 15, 38, 1218]
 
 
-@pytest.mark.parametrize("limit", ["1048576", "16777216", "10000000", "268435456", "4294967296", "1099511627776"])
-def test_families_match_reference(golden, limit):
+@pytest.mark.parametrize("limit", ["1048576", "16777216", "10000000", "268435456", "4294967296", "1099511627776",
+                                   "1400000000000"])
+def test_theorem1_oracle_matches_reference(golden, limit):
+    """oracle/theorem1.py (the checker used beyond CPU-search range) against the reference's
+    own expected_pairs_up_to rows (families.py:77-107), radicals included."""
+    from oracle import theorem1
+
     exp = golden["expected_pairs_up_to"][limit]
-    ks = bp.expected_pairs_up_to(int(limit))
-    assert rows_of(ks.first_kind) == exp["first"]
-    assert rows_of(ks.second_kind) == exp["second"]
+    got = theorem1.known_rows(int(limit))
+    assert [list(r) for r in got if r[0] == 1] == sorted(exp["first"], key=lambda r: (r[1], r[2]))
+    assert [list(r) for r in got if r[0] == 2] == sorted(exp["second"], key=lambda r: (r[1], r[2]))
 
 
 # ---------------------------------------------------------------- the lemma -----------------
@@ -200,6 +205,7 @@ def test_run_full_chunked_streaming_logic(orc, monkeypatch, golden):
         return _oracle_rows(orc, lo, hi)
 
     monkeypatch.setattr(chunked, "search_rows", fake)
+    monkeypatch.setattr(chunked, "_prepare_run", lambda *a: None)
     monkeypatch.setattr(chunked, "BATCH_INTEGERS", 50_000)
     for case in ("1048576_4096", "20000_64", "5000_300"):
         limit, s = (int(x) for x in case.split("_"))
