@@ -192,6 +192,8 @@ struct bnx_ctx {
     HeavyTab heavy_tab;
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
     bool trace = false;         // BNX_TRACE=1 (see Trace)
+    int stop_after = 0;         // profiling only (BNX_STOP_AFTER): run a prefix of the heavy pipeline
+    bool skip_readback = false; // profiling only (BNX_SKIP_READBACK): no D2H copy (results invalid)
     bool host_classes = false;  // BNX_HOST_CLASSES=1: the class table by the host DFS (tests)
     uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
     int heavy_grid = 0;       // tuning only (BNX_HEAVY_GRID, CTAs per SM); 0 = default
@@ -654,6 +656,7 @@ int ensure_work(bnx_ctx* c) {
 // PAIR_PREFIX pair rows (every search up to 2^48 has fewer: 49 of both kinds), so collect()
 // needs no second copy.
 int read_back(bnx_ctx* c) {
+    if (c->skip_readback) return BNX_OK;  // (profiling only)
     CK(cudaMemcpyAsync(c->h_io, c->io.p, IO_PAIRS + sizeof(bnx_pair_t) * c->pair_prefix, cudaMemcpyDeviceToHost,
                        c->stream));
     return BNX_OK;
@@ -809,7 +812,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
             CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
         }
         launch_heavy(ha, h.scan_temp.p, h.scan_bytes, grid, c->stream, nullptr, c->aux, c->fork_ev, c->join_ev,
-                     c->timing == 2 ? c->kev : nullptr);
+                     c->timing == 2 ? c->kev : nullptr, c->stop_after);
         CK(cudaGetLastError());
         return BNX_OK;
     };
@@ -817,6 +820,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // dependent of k_heavy_exact
     const bool single = c->use_graphs && !c->timing;
     auto record_tail = [&]() -> int {
+        if (c->stop_after) return read_back(c);  // (profiling: a prefix of the pipeline)
         // k_tail_heavy (the few candidates with many residue-class members) overlaps k_tail
         CK(cudaEventRecord(c->fork_ev, c->stream));
         CK(cudaStreamWaitEvent(c->aux, c->fork_ev, 0));
@@ -1087,6 +1091,8 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
+    if (const char* env = std::getenv("BNX_STOP_AFTER")) c->stop_after = std::atoi(env);
+    if (const char* env = std::getenv("BNX_SKIP_READBACK")) c->skip_readback = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_TRACE")) c->trace = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_HOST_CLASSES")) c->host_classes = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_HEAVY_KMIN")) c->heavy_kmin = std::strtoull(env, nullptr, 10);

@@ -826,7 +826,7 @@ size_t heavy_scan_temp_bytes(uint64_t nent) {
 
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
                   cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join,
-                  const cudaEvent_t* kev) {
+                  const cudaEvent_t* kev, int stop_after) {
     bool pdl = false;
     if (kev) cudaEventRecord(kev[0], st);
     if (a.nent) {
@@ -846,6 +846,10 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint32_t)) +
                              np2p * (sizeof(uint2) + sizeof(uint32_t));
         if (kev) cudaEventRecord(kev[1], st);
+        if (stop_after == 1) {
+            if (kev) for (int i = 2; i < 4; ++i) cudaEventRecord(kev[i], st);
+            return;
+        }
         k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
         pdl = !sieve && !kev;
@@ -853,6 +857,10 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         cudaEventRecord(kev[1], st);
     }
     if (kev) cudaEventRecord(kev[2], st);
+    if (stop_after == 2) {
+        if (kev) cudaEventRecord(kev[3], st);
+        return;
+    }
     const size_t np3p = (size_t)(a.np3 + 31) & ~(size_t)31;  // (see k_heavy_exact)
     const size_t smem3 = (size_t)a.np3 * (sizeof(ulonglong2) + sizeof(uint32_t)) + np3p * (sizeof(uint2) + sizeof(uint32_t));
     {  // a programmatic dependent launch right after k_heavy_screen (see k_heavy_exact)

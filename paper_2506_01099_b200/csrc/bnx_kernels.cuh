@@ -118,7 +118,8 @@ cudaError_t heavy_configure();
 size_t heavy_sieve_smem(int np2, int kc, int ntasks);
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
                   cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join,
-                  const cudaEvent_t* kev = nullptr);  // kev[0..3]: per-kernel timing (count, screen, exact)
+                  const cudaEvent_t* kev = nullptr,  // kev[0..3]: per-kernel timing (count, screen, exact)
+                  int stop_after = 0);  // profiling only: 1 = count + scan, 2 = + screen (0: all)
 
 // The surplus-class table built on the device (bnx_classes.cu).
 struct ClassPlan {
