@@ -520,13 +520,33 @@ __device__ __forceinline__ void div_slot(unsigned long long* s, uint64_t inv, bo
     } while (old != assumed);
 }
 
-template <int TILE, int NT, int THREADS, int BCAP, int MAXS, int MINB>
+// ASYNC: two tile buffers; a finished tile leaves through one bulk asynchronous copy
+// (cp.async.bulk shared -> global, issued by one thread, streaming L2 policy) while the
+// threads initialise the other buffer and run its progressions, so the HBM write stream
+// overlaps the next tile's compute and the warps issue no store instructions.
+__device__ __forceinline__ void bulk_store_tile(uint64_t* dst, const unsigned long long* src, uint32_t bytes) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(src);
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                 :: "l"(dst), "r"(s), "r"(bytes), "l"(pol) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {  // the issuing thread's groups but the newest N have read smem
+    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int TILE, int NT, int THREADS, int BCAP, int MAXS, int MINB, bool ASYNC>
 __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
     constexpr int NW = THREADS / 32;
     constexpr uint64_t SEG = (uint64_t)TILE * NT;
+    constexpr int NBUF = ASYNC ? 2 : 1;
     extern __shared__ __align__(16) unsigned long long sm64[];
-    unsigned long long* r = sm64;                        // TILE slots
-    unsigned long long* bent = r + TILE;                 // NT * BCAP : (p << 16 | loc)
+    unsigned long long* r0 = sm64;                       // NBUF * TILE slots
+    unsigned long long* bent = r0 + NBUF * TILE;         // NT * BCAP : (p << 16 | loc)
     unsigned long long* s_inv = bent + NT * BCAP;        // MAXS
     uint32_t* bcnt = (uint32_t*)(s_inv + MAXS);          // NT
     uint32_t* s_q = bcnt + NT;                           // MAXS (sorted by q on the host)
@@ -544,9 +564,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
     }
     for (int j = tid; j < nitems; j += THREADS) s_item[j] = a.items[j];
     const uint64_t nseg = (a.length + SEG - 1) / SEG;
+    int cur = 0;  // the buffer of the tile being sieved (ASYNC)
     for (uint64_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
         const uint64_t seg_off = seg * SEG;
         const uint64_t seg0 = a.start + seg_off;
+        if (ASYNC && tid == 0) bulk_wait_read<0>();  // (no store may still read the buffers)
         __syncthreads();
         for (int j = tid; j < NT; j += THREADS) bcnt[j] = 0;
         for (int j = tid; j < nsmall; j += THREADS) s_off[j] = (uint32_t)bnx_first_offset(seg0, s_q[j], a.small[j].recip);
@@ -567,7 +589,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
         // per thread and 16-byte stores: exactly one of them is even, and only that one can
         // need the shift.  Thread g always owns slots 2g, 2g+1 (init, write-out), so the
         // write-out of tile t and the init of tile t+1 share one pass with no barrier.
-        auto init_pair = [&](uint64_t tile0, int g) {
+        auto init_pair = [&](unsigned long long* buf, uint64_t tile0, int g) {
             const uint64_t x0 = tile0 + 2u * (uint32_t)g;
             uint64_t v0 = x0, v1 = x0 + 1;
             if (a.fast) {
@@ -580,12 +602,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
                     if (odd0) v1 = ve; else v0 = ve;
                 }
             }
-            reinterpret_cast<ulonglong2*>(r)[g] = make_ulonglong2(v0, v1);
+            reinterpret_cast<ulonglong2*>(buf)[g] = make_ulonglong2(v0, v1);
         };
-        for (int g = tid; g < TILE / 2; g += THREADS) init_pair(a.start + seg_off, g);
+        for (int g = tid; g < TILE / 2; g += THREADS) init_pair(r0 + cur * TILE, a.start + seg_off, g);
         for (int t = 0; t < NT; ++t) {
             const uint64_t toff = seg_off + (uint64_t)t * TILE;
             if (toff >= a.length) break;
+            unsigned long long* r = r0 + cur * TILE;
             __syncthreads();
             // per-tile progressions: balanced work items (see k_screen), exact division per hit
             const int it_end = (int)s_item[warp + 1];
@@ -622,26 +645,279 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
                 if (no < 0) no += (int)s_q[j];
                 s_off[j] = (uint32_t)no;
             }
-            // write out (16-byte streaming stores; the values are not re-read on the device)
-            // fused with the next tile's init
             const uint64_t rem = a.length - toff;
             const int lim = rem < (uint64_t)TILE ? (int)rem : TILE;
             uint64_t* dst = a.out + toff;
             const bool next = t + 1 < NT && toff + TILE < a.length;
-            if (lim == TILE && ((((uintptr_t)dst) & 15) == 0)) {
+            const bool whole = lim == TILE && ((((uintptr_t)dst) & 15) == 0);
+            if (ASYNC) {
+                unsigned long long* rn = r0 + (cur ^ 1) * TILE;
+                if (whole) {
+                    if (tid == 0) {
+                        bulk_store_tile(dst, r, TILE * 8u);
+                        bulk_wait_read<1>();  // the other buffer's store (one tile ago) has read it
+                    }
+                    __syncthreads();
+                    if (next)
+                        for (int g = tid; g < TILE / 2; g += THREADS) init_pair(rn, a.start + toff + TILE, g);
+                } else {  // ragged last tile or an output only 8-byte aligned: plain stores
+                    if (tid == 0) bulk_wait_read<0>();
+                    __syncthreads();
+                    for (int g = tid; g < TILE / 2; g += THREADS) {
+                        if (2 * g < lim) dst[2 * g] = r[2 * g];
+                        if (2 * g + 1 < lim) dst[2 * g + 1] = r[2 * g + 1];
+                        if (next) init_pair(rn, a.start + toff + TILE, g);
+                    }
+                }
+                cur ^= 1;
+            } else if (whole) {
+                // write out (16-byte streaming stores; the values are not re-read on the device)
+                // fused with the next tile's init
                 for (int g = tid; g < TILE / 2; g += THREADS) {
                     __stcs(reinterpret_cast<ulonglong2*>(dst) + g, reinterpret_cast<const ulonglong2*>(r)[g]);
-                    if (next) init_pair(a.start + toff + TILE, g);
+                    if (next) init_pair(r, a.start + toff + TILE, g);
                 }
             } else {  // ragged last tile or an output only 8-byte aligned: same slot ownership
                 for (int g = tid; g < TILE / 2; g += THREADS) {
                     if (2 * g < lim) dst[2 * g] = r[2 * g];
                     if (2 * g + 1 < lim) dst[2 * g + 1] = r[2 * g + 1];
-                    if (next) init_pair(a.start + toff + TILE, g);
+                    if (next) init_pair(r, a.start + toff + TILE, g);
                 }
             }
         }
     }
+    if (ASYNC && tid == 0) bulk_wait_all();  // (the last stores complete before the kernel retires)
+}
+
+// ---- k_sieve_pipe: the same sieve as a barrier-free software pipeline --------------------
+// k_sieve_exact synchronises the whole CTA twice per tile, and a third of its stall samples
+// wait at the barrier behind the slowest warp's progressions.  Here the tiles of a CTA run
+// through three shared-memory buffers with mbarriers instead of CTA barriers:
+//   compute warps (NWC)  wait ready[b] -> progressions + buckets of tile k -> arrive full[b]
+//                        -> wait freed (tile k-1's buffer) -> initialise their slice of tile
+//                        k+2 (values and progression offsets) -> arrive ready
+//   store warp (1)       wait full[b] -> one bulk asynchronous copy of the tile to HBM
+//                        (cp.async.bulk, streaming L2 policy) -> wait for its shared-memory
+//                        read -> arrive freed[b]
+// so a warp can run up to a tile ahead of the slowest one and the HBM stream never waits for
+// a barrier.  Large-progression buckets are double-buffered per segment: the compute warps
+// fill segment i+1's set while they start segment i.
+namespace pipe {
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void init(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(sa(bar)), "r"(parity) : "memory");
+}
+}  // namespace pipe
+
+template <int TILE, int NT, int NWC, int BCAP, int MAXS>
+__global__ void __launch_bounds__(NWC * 32 + 32, 1) k_sieve_pipe(SieveArgs a) {
+    constexpr int TC = NWC * 32;  // compute threads
+    constexpr uint64_t SEG = (uint64_t)TILE * NT;
+    constexpr int PAIRS_W = TILE / 2 / NWC;  // init pairs per compute warp
+    static_assert(TILE / 2 % NWC == 0, "the compute warps must split the tile's pairs evenly");
+    extern __shared__ __align__(16) unsigned long long sm64[];
+    unsigned long long* buf = sm64;                                    // 3 * TILE
+    unsigned long long* bent = buf + 3 * TILE;                         // 2 * NT * BCAP
+    unsigned long long* s_inv = bent + 2 * NT * BCAP;                  // MAXS
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_inv + MAXS);        // ready[3] full[3] freed[3] bready[2] bfree[2]
+    uint32_t* bcnt = reinterpret_cast<uint32_t*>(bars + 16);           // 2 * NT
+    uint32_t* s_q = bcnt + 2 * NT;                                     // MAXS
+    uint32_t* s_tm = s_q + MAXS;                                       // MAXS
+    uint32_t* s_base = s_tm + MAXS;                                    // 2 * MAXS (segment start offsets)
+    uint32_t* s_off = s_base + 2 * MAXS;                               // 3 * MAXS (per buffer)
+    uint32_t* s_item = s_off + 3 * MAXS;                               // 2 * MAXS work items
+    uint64_t* ready = bars;
+    uint64_t* full = bars + 3;
+    uint64_t* freed = bars + 6;
+    uint64_t* bready = bars + 9;
+    uint64_t* bfree = bars + 11;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nsmall = a.nsmall, nitems = a.nitems;
+    for (int j = tid; j < nsmall; j += blockDim.x) {
+        const uint32_t q = (uint32_t)a.small[j].q, p = a.small[j].p;
+        s_q[j] = q;
+        s_tm[j] = (uint32_t)TILE % q;
+        s_inv[j] = (p == 2) ? 0ull : bnx_inv64(p);
+    }
+    for (int j = tid; j < nitems; j += blockDim.x) s_item[j] = a.items[j];
+    for (int j = tid; j < 2 * NT; j += blockDim.x) bcnt[j] = 0;
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) {
+            pipe::init(ready + b, NWC);
+            pipe::init(full + b, NWC);
+            pipe::init(freed + b, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            pipe::init(bready + s, NWC);
+            pipe::init(bfree + s, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // this CTA's tiles: segments blockIdx.x + i * gridDim.x, each up to NT tiles of the input
+    const uint64_t nseg_all = (a.length + SEG - 1) / SEG;
+    const uint64_t nseg = blockIdx.x < nseg_all ? (nseg_all - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto seg_off_of = [&](uint64_t i) { return (blockIdx.x + i * gridDim.x) * SEG; };
+    auto tiles_of = [&](uint64_t i) {
+        const uint64_t rem = a.length - seg_off_of(i);
+        return (int)min((uint64_t)NT, (rem + TILE - 1) / TILE);
+    };
+    if (nseg == 0) return;
+    // tile k (CTA order) -> (segment, tile in segment): every segment but the last has NT tiles
+    const uint64_t ktotal = (nseg - 1) * NT + (uint64_t)tiles_of(nseg - 1);
+    auto seg_of = [&](uint64_t k) { return k / NT; };
+    auto jt_of = [&](uint64_t k) { return (int)(k % NT); };
+
+    if (warp == NWC) {  // ---------------------------------------------- store warp
+        for (uint64_t k = 0; k < ktotal; ++k) {
+            const int b = (int)(k % 3);
+            pipe::wait(full + b, (uint32_t)((k / 3) & 1));
+            const uint64_t i = seg_of(k);
+            const int jt = jt_of(k);
+            const uint64_t toff = seg_off_of(i) + (uint64_t)jt * TILE;
+            const uint64_t rem = a.length - toff;
+            const int lim = rem < (uint64_t)TILE ? (int)rem : TILE;
+            uint64_t* dst = a.out + toff;
+            const unsigned long long* r = buf + b * TILE;
+            if (lim == TILE && ((((uintptr_t)dst) & 15) == 0)) {
+                if (lane == 0) {
+                    bulk_store_tile(dst, r, TILE * 8u);
+                    bulk_wait_read<0>();
+                }
+            } else {
+                for (int g = lane; g < lim; g += 32) dst[g] = r[g];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                bcnt[(i & 1) * NT + jt] = 0;  // this tile's bucket slot, ready for segment i + 2
+                pipe::arrive(freed + b);
+                if (jt == tiles_of(i) - 1) pipe::arrive(bfree + (i & 1));
+            }
+        }
+        if (lane == 0) bulk_wait_all();
+        return;
+    }
+
+    // ------------------------------------------------------------------ compute warps
+    // bucket fill (large progressions) and segment start offsets (small ones) for segment i,
+    // shared by all compute threads; set i & 1 must be free (segment i - 2 consumed)
+    auto fill = [&](uint64_t i) {
+        const int set = (int)(i & 1);
+        if (i >= 2) pipe::wait(bfree + set, (uint32_t)(((i - 2) >> 1) & 1));
+        const uint64_t seg0 = a.start + seg_off_of(i);
+        for (uint64_t j = tid; j < a.nlarge; j += TC) {
+            const BnxProg pr = a.large[j];
+            uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip);
+            while (o < SEG) {
+                const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
+                const uint32_t kk = atomicAdd(&bcnt[set * NT + t], 1u);
+                if (kk < BCAP) bent[(set * NT + t) * BCAP + kk] = ((uint64_t)pr.p << 16) | loc; else a.flags[0] = 1;
+                if (pr.q >= SEG) break;
+                o += pr.q;
+            }
+        }
+        for (int j = tid; j < nsmall; j += TC) s_base[set * MAXS + j] = (uint32_t)bnx_first_offset(seg0, s_q[j], a.small[j].recip);
+        __syncwarp();
+        if (lane == 0) pipe::arrive(bready + set);
+    };
+    // this warp's slice of tile k: values (or the ctz-stripped values) and a share of the
+    // progression offsets; the buffer must have been read out by the store of tile k - 3
+    auto prepare = [&](uint64_t k) {
+        const int b = (int)(k % 3);
+        if (k >= 3) pipe::wait(freed + b, (uint32_t)(((k - 3) / 3) & 1));
+        const uint64_t i = seg_of(k);
+        const int jt = jt_of(k);
+        const uint64_t tile0 = a.start + seg_off_of(i) + (uint64_t)jt * TILE;
+        unsigned long long* r = buf + b * TILE;
+        for (int g = warp * PAIRS_W + lane; g < (warp + 1) * PAIRS_W; g += 32) {
+            const uint64_t x0 = tile0 + 2u * (uint32_t)g;
+            uint64_t v0 = x0, v1 = x0 + 1;
+            if (a.fast) {
+                const bool odd0 = x0 & 1;
+                const uint64_t xe = odd0 ? v1 : v0;
+                if ((xe & 3) == 0 && xe) {
+                    const uint32_t lo = (uint32_t)xe;
+                    const int tz = lo ? __ffs(lo) - 1 : 31 + __ffs((uint32_t)(xe >> 32));
+                    const uint64_t ve = xe >> (tz - 1);
+                    if (odd0) v1 = ve; else v0 = ve;
+                }
+            }
+            reinterpret_cast<ulonglong2*>(r)[g] = make_ulonglong2(v0, v1);
+        }
+        pipe::wait(bready + (i & 1), (uint32_t)((i >> 1) & 1));  // (segment i's start offsets)
+        for (int j = warp * 32 + lane; j < nsmall; j += TC) {
+            const uint32_t q = s_q[j];
+            const uint32_t back = (uint32_t)(((uint64_t)jt * s_tm[j]) % q);
+            uint32_t o = s_base[(i & 1) * MAXS + j] + q - back;
+            if (o >= q) o -= q;
+            s_off[b * MAXS + j] = o;
+        }
+        __syncwarp();
+        if (lane == 0) pipe::arrive(ready + b);
+    };
+
+    fill(0);
+    prepare(0);
+    if (ktotal > 1) prepare(1);
+    for (uint64_t k = 0; k < ktotal; ++k) {
+        const int b = (int)(k % 3);
+        const uint64_t i = seg_of(k);
+        const int jt = jt_of(k);
+        // (segment i+1's set is free once segment i-1 has been stored: a few tiles into i)
+        if (i + 1 < nseg && jt == min(2, tiles_of(i) - 1)) fill(i + 1);
+        pipe::wait(ready + b, (uint32_t)((k / 3) & 1));
+        unsigned long long* r = buf + b * TILE;
+        const uint32_t* off = s_off + b * MAXS;
+        const int it_end = (int)s_item[warp + 1];
+        for (int it = (int)s_item[warp]; it < it_end; ++it) {
+            const uint32_t e = s_item[NWC + 1 + it];
+            const int j = (int)(e & 0xFFu);
+            if (e >> 31) {
+                const int jj = j + lane;
+                if (jj < nsmall) {
+                    const uint32_t q = s_q[jj];
+                    const uint64_t inv = s_inv[jj];
+                    for (uint32_t o = off[jj]; o < TILE; o += q) div_slot(&r[o], inv, inv == 0);
+                }
+            } else {
+                const uint32_t rr = (e >> 8) & 0xFFu, R = (e >> 16) & 0x7FFFu;
+                const uint32_t q = s_q[j];
+                const uint64_t inv = s_inv[j];
+                const uint32_t step = 32u * R * q;
+                for (uint32_t o = off[j] + (rr * 32u + (uint32_t)lane) * q; o < TILE; o += step)
+                    div_slot(&r[o], inv, inv == 0);
+            }
+        }
+        {
+            const int set = (int)(i & 1);
+            const uint32_t nb = min(bcnt[set * NT + jt], (uint32_t)BCAP);
+            for (uint32_t t = tid; t < nb; t += TC) {
+                const unsigned long long e = bent[(set * NT + jt) * BCAP + t];
+                const uint32_t p = (uint32_t)(e >> 16);
+                div_slot(&r[e & 0xFFFFu], p == 2 ? 0ull : bnx_inv64(p), p == 2);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) pipe::arrive(full + b);
+        if (k + 2 < ktotal) prepare(k + 2);
+    }
+}
+
+template <int TILE, int NT, int NWC, int BCAP>
+constexpr size_t sieve_pipe_smem() {
+    return sizeof(unsigned long long) * ((size_t)3 * TILE + (size_t)2 * NT * BCAP + SIEVE_MAXS) + 16 * 8 +
+           sizeof(uint32_t) * ((size_t)2 * NT + 9 * SIEVE_MAXS);
 }
 
 // _kernels.py:87-112 on the GPU: one thread per integer, trial division by the odd primes.
@@ -771,25 +1047,40 @@ __global__ void k_table_probe(TableArgs a) {
 
 // ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
-template <int TILE, int NT, int BCAP>
+template <int TILE, int NT, int BCAP, bool ASYNC = false>
 constexpr size_t sieve_smem() {
-    return sizeof(unsigned long long) * ((size_t)TILE + (size_t)NT * BCAP + SIEVE_MAXS) +
+    return sizeof(unsigned long long) * ((size_t)TILE * (ASYNC ? 2 : 1) + (size_t)NT * BCAP + SIEVE_MAXS) +
            sizeof(uint32_t) * ((size_t)NT + 5 * SIEVE_MAXS);
 }
-template <int TILE, int NT, int THREADS, int BCAP, int MINB>
+template <int TILE, int NT, int THREADS, int BCAP, int MINB, bool ASYNC>
 void launch_sieve_v(const SieveArgs& a, int grid, cudaStream_t st) {
-    k_sieve_exact<TILE, NT, THREADS, BCAP, SIEVE_MAXS, MINB><<<grid, THREADS, sieve_smem<TILE, NT, BCAP>(), st>>>(a);
+    k_sieve_exact<TILE, NT, THREADS, BCAP, SIEVE_MAXS, MINB, ASYNC>
+        <<<grid, THREADS, sieve_smem<TILE, NT, BCAP, ASYNC>(), st>>>(a);
 }
-#define BNX_SIEVE_VARIANT(T, N, H, B, M)                                                                   \
-    SieveVariant{T, N, H, B, (const void*)k_sieve_exact<T, N, H, B, SIEVE_MAXS, M>, sieve_smem<T, N, B>(), \
-                 launch_sieve_v<T, N, H, B, M>}
+template <int TILE, int NT, int NWC, int BCAP>
+void launch_sieve_pipe(const SieveArgs& a, int grid, cudaStream_t st) {
+    k_sieve_pipe<TILE, NT, NWC, BCAP, SIEVE_MAXS><<<grid, NWC * 32 + 32, sieve_pipe_smem<TILE, NT, NWC, BCAP>(), st>>>(a);
+}
+#define BNX_SIEVE_VARIANT(T, N, H, B, M, A)                                                                    \
+    SieveVariant{T, N, H, B, (const void*)k_sieve_exact<T, N, H, B, SIEVE_MAXS, M, A>, sieve_smem<T, N, B, A>(), \
+                 launch_sieve_v<T, N, H, B, M, A>}
 static const SieveVariant kSieveVariants[] = {
     // default; the others measured slower on [1, 2^30] (scripts/sieve_variants.py,
     // profiles/r01_sieve_variants.jsonl): 2.18 ms against 2.44, 2.62, 2.78
-    BNX_SIEVE_VARIANT(SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, 2),
-    BNX_SIEVE_VARIANT(8192, 64, 768, 64, 2),
-    BNX_SIEVE_VARIANT(8192, 64, 256, 64, 4),
-    BNX_SIEVE_VARIANT(4096, 64, 512, 48, 3),
+    BNX_SIEVE_VARIANT(SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, 2, false),
+    BNX_SIEVE_VARIANT(8192, 64, 768, 64, 2, false),
+    BNX_SIEVE_VARIANT(8192, 64, 256, 64, 4, false),
+    BNX_SIEVE_VARIANT(4096, 64, 512, 48, 3, false),
+    // bulk asynchronous write-out from a second tile buffer (see bulk_store_tile): one CTA
+    // per SM fits two 64 KB tiles, and the lost second CTA costs more than the stores save
+    // (3.41 / 3.35 ms on [1, 2^30]; 4096-slot tiles with two CTAs: 3.28 ms async, 3.84 ms not)
+    BNX_SIEVE_VARIANT(8192, 64, 1024, 64, 1, true),
+    BNX_SIEVE_VARIANT(8192, 64, 512, 64, 1, true),
+    // the barrier-free pipeline (k_sieve_pipe): 16 compute warps + a store warp, one CTA per
+    // SM (three 64 KB tiles): no barrier stalls, but too few warps to hide the shared-memory
+    // CAS latency (3.84 ms on [1, 2^30] against 2.17 ms for variant 0)
+    SieveVariant{8192, 24, 512, 64, (const void*)k_sieve_pipe<8192, 24, 16, 64, SIEVE_MAXS>,
+                 sieve_pipe_smem<8192, 24, 16, 64>(), launch_sieve_pipe<8192, 24, 16, 64>},
 };
 int sieve_variant_count() { return (int)(sizeof(kSieveVariants) / sizeof(kSieveVariants[0])); }
 const SieveVariant& sieve_variant(int i) { return kSieveVariants[i]; }

@@ -54,8 +54,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "child":
         child()
     else:
-        nv = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-        for v in list(range(nv)) + [0]:
+        arg = sys.argv[1] if len(sys.argv) > 1 else "4"  # a count, or a comma-separated list
+        vs = [int(v) for v in arg.split(",")] if "," in arg else list(range(int(arg))) + [0]
+        for v in vs:
             env = dict(os.environ, BNX_SIEVE_VARIANT=str(v))
             r = subprocess.run([sys.executable, __file__, "child"], env=env, capture_output=True, text=True)
             print(r.stdout.strip() or f'{{"variant": {v}, "error": {json.dumps(r.stderr[-400:])}}}', flush=True)
