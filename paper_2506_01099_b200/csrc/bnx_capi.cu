@@ -193,6 +193,7 @@ struct bnx_ctx {
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
     bool trace = false;         // BNX_TRACE=1 (see Trace)
     int stop_after = 0;         // profiling only (BNX_STOP_AFTER): run a prefix of the heavy pipeline
+    int table_lanes = 1;        // Algorithm 3: lanes per element (BNX_TABLE_LANES: 1 or 4; 4 measured slower)
     bool skip_readback = false; // profiling only (BNX_SKIP_READBACK): no D2H copy (results invalid)
     bool host_classes = false;  // BNX_HOST_CLASSES=1: the class table by the host DFS (tests)
     uint64_t heavy_kmin = 0;  // tuning only (BNX_HEAVY_KMIN); 0 = default
@@ -1092,6 +1093,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
     if (const char* env = std::getenv("BNX_STOP_AFTER")) c->stop_after = std::atoi(env);
+    if (const char* env = std::getenv("BNX_TABLE_LANES")) c->table_lanes = std::atoi(env) == 4 ? 4 : 1;
     if (const char* env = std::getenv("BNX_SKIP_READBACK")) c->skip_readback = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_TRACE")) c->trace = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_HOST_CLASSES")) c->host_classes = std::atoi(env) != 0;
@@ -1520,8 +1522,8 @@ static int table_run(bnx_table* tb, bool insert, uint64_t a0, uint64_t count, ui
         ta.inserted = tb->cnt.p + 1;
         ta.status = tb->status.p;
         const int grid = c->num_sms * 8;
-        if (insert) launch_table_insert(ta, grid, c->stream);
-        else launch_table_probe(ta, grid, c->stream);
+        if (insert) launch_table_insert(ta, grid, c->stream, c->table_lanes);
+        else launch_table_probe(ta, grid, c->stream, c->table_lanes);
         CK(cudaGetLastError());
         unsigned long long h[2] = {0, 0};
         int st = 0;

@@ -1045,6 +1045,67 @@ __global__ void k_table_probe(TableArgs a) {
     }
 }
 
+// The paper's parallel probe ("examine the slot at the initial address, the
+// next one, and so on ... the best performance was achieved by examining 4 addresses in
+// parallel"): four lanes per element read four consecutive slots at once; every slot before
+// the first empty one is checked for an equal signature, and insert claims that empty slot
+// by CAS (a lost race re-reads from it: its new occupant may match).  Same pairs, same
+// slot words and probe sequences as the one-lane kernels above.
+template <bool INSERT>
+__global__ void __launch_bounds__(256) k_table_quad(TableArgs a) {
+    const int lane = threadIdx.x & 31, q = lane & 3;
+    const unsigned qmask = 0xFu << (lane & ~3);
+    const uint64_t nq = ((uint64_t)gridDim.x * blockDim.x) >> 2;
+    const uint64_t count = INSERT ? a.count_n : a.count_m;
+    const uint64_t* of = INSERT ? a.rad_of : a.probe_of;
+    const uint64_t* nx = INSERT ? a.rad_next : a.probe_next;
+    for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 2; t < count; t += nq) {
+        if (INSERT && a.domain_start + t >= a.n_limit) continue;  // (quad-uniform)
+        const uint64_t x = of[t], y = nx[t];
+        const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
+        const uint64_t home = table_slot_of(lo, hi, a.mask);
+        const unsigned long long mine = ((unsigned long long)(t + 1) << 32) | home;
+        uint64_t idx = home, steps = 0;
+        for (;;) {
+            const uint64_t slot = (idx + q) & a.mask;
+            const unsigned long long stored = a.slots[slot];
+            const unsigned emp = (__ballot_sync(qmask, stored == 0) >> (lane & ~3)) & 0xFu;
+            const int fe = emp ? __ffs(emp) - 1 : 4;  // first empty slot of the window
+            if (q < fe && (stored & 0xFFFFFFFFull) == home) {
+                const uint64_t tp = (stored >> 32) - 1;
+                const uint64_t x2 = a.rad_of[tp], y2 = a.rad_next[tp];
+                if ((x2 < y2 ? x2 : y2) == lo && (x2 < y2 ? y2 : x2) == hi) {
+                    if (INSERT) {
+                        const uint64_t tm = tp < t ? tp : t, tn = tp < t ? t : tp;
+                        const uint64_t rm = a.rad_of[tm], rm1 = a.rad_next[tm];
+                        table_emit(a, rm == a.rad_of[tn] ? 1 : 2, a.domain_start + tm, a.domain_start + tn, rm, rm1);
+                    } else {
+                        table_emit(a, x == x2 ? 1 : 2, a.probe_start + t, a.domain_start + tp, x, y);
+                    }
+                }
+            }
+            if (fe < 4) {
+                if (!INSERT) break;
+                unsigned long long won = 1;
+                if (q == fe) {
+                    won = atomicCAS(reinterpret_cast<unsigned long long*>(a.slots) + slot, 0ull, mine) == 0ull;
+                    if (won) atomicAdd(a.inserted, 1ull);
+                }
+                if (__shfl_sync(qmask, won, (lane & ~3) + fe)) break;
+                idx += fe;  // lost the slot: look at its new occupant and on from there
+                steps += fe;
+            } else {
+                idx += 4;
+                steps += 4;
+            }
+            if (steps > a.mask) {
+                if (q == 0) *a.status = BNX_TABLE_FULL;
+                break;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
 template <int TILE, int NT, int BCAP, bool ASYNC = false>
@@ -1156,8 +1217,14 @@ void launch_brute_force(const uint64_t* rads, uint64_t limit, bnx_pair_t* out, u
     const uint64_t blocks = (limit + 255) / 256;
     k_brute_force<<<(unsigned)blocks, 256, 0, st>>>(rads, limit, out, cap, count);
 }
-void launch_table_insert(const TableArgs& a, int grid, cudaStream_t st) { k_table_insert<<<grid, 256, 0, st>>>(a); }
-void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st) { k_table_probe<<<grid, 256, 0, st>>>(a); }
+void launch_table_insert(const TableArgs& a, int grid, cudaStream_t st, int lanes) {
+    if (lanes == 4) k_table_quad<true><<<grid, 256, 0, st>>>(a);
+    else k_table_insert<<<grid, 256, 0, st>>>(a);
+}
+void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st, int lanes) {
+    if (lanes == 4) k_table_quad<false><<<grid, 256, 0, st>>>(a);
+    else k_table_probe<<<grid, 256, 0, st>>>(a);
+}
 void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, uint64_t npd, uint64_t* out,
                            int grid, cudaStream_t st) {
     k_trial_division<<<grid, 256, 0, st>>>(start, length, pd, npd, out);

@@ -182,8 +182,9 @@ struct TableArgs {
     unsigned long long* inserted;
     int* status;
 };
-void launch_table_insert(const TableArgs& a, int grid, cudaStream_t st);
-void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st);
+// lanes: 1 (a thread per element) or 4 (the paper's four-slot parallel probe, k_table_quad)
+void launch_table_insert(const TableArgs& a, int grid, cudaStream_t st, int lanes);
+void launch_table_probe(const TableArgs& a, int grid, cudaStream_t st, int lanes);
 // Compiled exact-sieve geometries (tile, tiles per segment, threads, bucket capacity); the
 // context picks one at creation (BNX_SIEVE_VARIANT, default 0).
 struct SieveVariant {

@@ -189,3 +189,51 @@ def test_rows_beyond_the_read_back_prefix(prefix, golden):
     exp = golden["expected_pairs_up_to"]["4294967296"]
     assert json.loads(out.stdout.strip().splitlines()[-1]) == sorted(exp["first"] + exp["second"],
                                                                       key=lambda r: (r[1], r[2]))
+
+
+def test_smallest_limits_with_a_caller_prime_list():
+    """limit 3 (isqrt = 1: the supplied list covers it with no primes at all) returns the
+    reference's empty result instead of failing in the table build; 4 and 10 stay golden."""
+    import paper_2506_01099_b200 as bp
+
+    for lim in (3, 4):
+        assert bp.find_pairs_sorted(lim, bp.primes_up_to(1)) == []
+        assert bp.find_pairs_sorted(lim, bp.primes_up_to(2)) == []
+    assert [(int(p.kind), p.m, p.n) for p in bp.find_pairs_sorted(10, bp.primes_up_to(3))] == \
+        [(2, 2, 3), (1, 2, 8), (2, 3, 8)]
+    assert bp.search_chunk(0, 3, bp.primes_up_to(1), n_limit=3) == []
+    assert list(bp.run_full_chunked(3, 3, bp.primes_up_to(1))) == []
+
+
+def test_collect_keeps_rows_after_buffer_full():
+    """bnx_search_collect answering BNX_BUFFER_FULL keeps the rows: the retry with a large
+    enough buffer returns them (no 'no search enqueued')."""
+    L = _native.load()
+    ctx = _native.Context(0)
+    try:
+        ctx.prepare(2**32)
+        ctx.enqueue(1, 2**32 - 1, 3)
+        found = ctypes.c_size_t(0)
+        small = (_native.PairRow * 2)()
+        assert L.bnx_search_collect(ctx.handle, small, 2, ctypes.byref(found)) == _native.BNX_BUFFER_FULL
+        assert found.value == 33
+        big = (_native.PairRow * 33)()
+        assert L.bnx_search_collect(ctx.handle, big, 33, ctypes.byref(found)) == _native.BNX_OK
+        assert found.value == 33 and sorted((r.m, r.n) for r in big)[0] == (2, 3)
+    finally:
+        ctx.close()
+
+
+def test_table_search_chunk_refuses_oversized_tables():
+    """chunk_size - 1 > 2^30 would need more than 2^32 slots (32-bit home slots); refused
+    like the reference's SignatureTable (chunked.py:157-158) instead of dropping pairs."""
+    import paper_2506_01099_b200 as bp
+
+    with pytest.raises(ValueError):
+        bp.search_chunk_table(0, (1 << 30) + 2)
+    L = _native.load()
+    ctx = _native.context(0)
+    found = ctypes.c_size_t(0)
+    buf = (_native.PairRow * 4)()
+    assert L.bnx_table_search_chunk(ctx.handle, 0, (1 << 30) + 2, 2**40, 0, 0, buf, 4,
+                                    ctypes.byref(found)) == _native.BNX_ERR_INVALID
