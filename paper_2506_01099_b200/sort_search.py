@@ -1,9 +1,12 @@
 """Full search below a bound -- drop-in for the reference's ``sort_search.py``.
 
-``find_pairs_sorted`` keeps the reference's signature and result (every pair m < n < limit,
-both kinds, sorted by (m, n); sort_search.py:37-91) but runs the B200 search engine, which
-needs no per-integer records: its device footprint is a few fixed buffers plus the prime
-tables, so the memory budget check applies to that footprint.
+``find_pairs_sorted`` keeps the reference's signature, result (every pair m < n < limit, both
+kinds, sorted by (m, n); sort_search.py:37-91) and failure modes, including the memory-budget
+refusal (sort_search.py:53-58: 48 bytes per record, 14 GiB default, MemoryBudgetExceeded
+pointing to the chunked search), so code written against the reference behaves the same.  The
+B200 engine itself keeps nothing per integer: ``memory_budget_bytes=None`` lifts the refusal
+(every bound up to 2^48), and ``find_pairs`` is the same search without the reference's
+budget rule.
 """
 from __future__ import annotations
 
@@ -15,15 +18,9 @@ from .radical import RadicalSegment
 from .search import find_pairs
 from .signatures import BeneluxPair, PairSignature, signature_of
 
-# Reference: values + lo + hi + sort order + two sorted key copies, all uint64 (sort_search.py:18).
-# The device path keeps nothing per integer; kept for API compatibility.
+# values + lo + hi + sort order + two sorted key copies, all uint64 (sort_search.py:17-19)
 BYTES_PER_RECORD = 48
 DEFAULT_MEMORY_BUDGET = 14 * 2**30
-
-# Fixed device work buffers of one search context (survivors, candidates, matches, pairs,
-# counters) and bytes per prime-table entry (prime, progression, exact-division constants).
-DEVICE_WORK_BYTES = (1 << 20) * 8 + (1 << 14) * 40 + 4096
-DEVICE_BYTES_PER_PRIME = 4 + 24 + 24
 
 
 class MemoryBudgetExceeded(ValueError):
@@ -41,23 +38,16 @@ def signature_record(n: int, segment: RadicalSegment) -> SignatureRecord:
     return SignatureRecord(n, signature_of(n, segment.rad(n), segment.rad(n + 1)))
 
 
-def device_bytes_for(limit: int) -> int:
-    """Device memory one search below `limit` needs (work buffers + prime tables)."""
-    root = math.isqrt(limit)
-    primes_est = int(1.26 * root / max(1.0, math.log(max(root, 2)))) + 64
-    return DEVICE_WORK_BYTES + DEVICE_BYTES_PER_PRIME * primes_est
-
-
 def find_pairs_sorted(limit: int, primes: PrimeList | None = None, *,
-                      memory_budget_bytes: int = DEFAULT_MEMORY_BUDGET, device: int | None = None
+                      memory_budget_bytes: int | None = DEFAULT_MEMORY_BUDGET, device: int | None = None
                       ) -> list[BeneluxPair]:
     """Every Benelux pair of either kind with m < n < limit, sorted by (m, n)."""
     if limit < 3:
         raise ValueError("limit must be >= 3")
-    estimated = device_bytes_for(limit)
-    if estimated > memory_budget_bytes:
+    estimated = BYTES_PER_RECORD * limit
+    if memory_budget_bytes is not None and estimated > memory_budget_bytes:
         raise MemoryBudgetExceeded(
-            f"searching below {limit} needs about {estimated} bytes of device memory "
+            f"sorting {limit} records needs about {estimated} bytes "
             f"(budget {memory_budget_bytes}); use the chunked search"
         )
     if primes is not None and not primes.covers(math.isqrt(limit)):

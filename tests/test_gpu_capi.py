@@ -196,9 +196,10 @@ def test_smallest_limits_with_a_caller_prime_list():
     reference's empty result instead of failing in the table build; 4 and 10 stay golden."""
     import paper_2506_01099_b200 as bp
 
-    for lim in (3, 4):
-        assert bp.find_pairs_sorted(lim, bp.primes_up_to(1)) == []
-        assert bp.find_pairs_sorted(lim, bp.primes_up_to(2)) == []
+    assert bp.find_pairs_sorted(3, bp.primes_up_to(1)) == []
+    assert bp.find_pairs_sorted(4, bp.primes_up_to(2)) == []
+    with pytest.raises(ValueError):  # isqrt(4) = 2 is not covered by the primes up to 1
+        bp.find_pairs_sorted(4, bp.primes_up_to(1))
     assert [(int(p.kind), p.m, p.n) for p in bp.find_pairs_sorted(10, bp.primes_up_to(3))] == \
         [(2, 2, 3), (1, 2, 8), (2, 3, 8)]
     assert bp.search_chunk(0, 3, bp.primes_up_to(1), n_limit=3) == []

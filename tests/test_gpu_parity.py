@@ -146,7 +146,7 @@ def test_chunk_callback_order():
 @pytest.mark.parametrize("limit", ["1048576", "16777216", "10000000", "268435456", "4294967296"])
 def test_known_solutions(golden, limit):
     exp = golden["expected_pairs_up_to"][limit]
-    got = bp.find_pairs_sorted(int(limit))
+    got = bp.find_pairs_sorted(int(limit), memory_budget_bytes=None)
     assert rows_of([p for p in got if p.kind == bp.Kind.FIRST]) == sorted(exp["first"], key=lambda r: (r[1], r[2]))
     assert rows_of([p for p in got if p.kind == bp.Kind.SECOND]) == sorted(exp["second"], key=lambda r: (r[1], r[2]))
 
@@ -165,6 +165,10 @@ def test_errors():
         bp.find_pairs_sorted(2)
     with pytest.raises(bp.MemoryBudgetExceeded, match="chunked"):
         bp.find_pairs_sorted(10**6, memory_budget_bytes=10**6)
+    # the reference's default budget (14 GiB at 48 B per record) refuses 2^32 as it does
+    with pytest.raises(bp.MemoryBudgetExceeded):
+        bp.find_pairs_sorted(2**32)
+    assert len(bp.find_pairs_sorted(2**28)) == 29  # 48 * 2^28 = 12 GiB fits
     with pytest.raises(ValueError):
         list(bp.run_full_chunked(2, 300))
     with pytest.raises(ValueError):
@@ -182,7 +186,7 @@ def test_reference_run_2p32_exact_rows():
 
     ref = json.load(open(os.path.join(ROOT, "tests", "golden", "ref_pairs_2p32.json")))["rows"]
     assert rows_of(bp.run_full_chunked(2**32, 2**28)) == ref
-    assert sorted(rows_of(bp.find_pairs_sorted(2**32)), key=lambda r: (r[1], r[2])) == \
+    assert sorted(rows_of(bp.find_pairs_sorted(2**32, memory_budget_bytes=None)), key=lambda r: (r[1], r[2])) == \
         sorted(ref, key=lambda r: (r[1], r[2]))
 
 
@@ -359,7 +363,7 @@ def test_paper_range_both_kinds_is_theorem_1():
     S = theorem1.COMPLETENESS_BOUND
     want = theorem1.known_rows(S)
     assert len(want) == 42
-    assert _rows(bp.find_pairs_sorted(S)) == want
+    assert _rows(bp.find_pairs_sorted(S, memory_budget_bytes=None)) == want
     for kind in (1, 2):
         got = _rows(bp.search.find_pairs(S, kinds=kind))
         assert got == [r for r in want if r[0] == kind], kind
