@@ -63,3 +63,35 @@ def test_single_thread_multi_device_search(devices, golden):
     assert got == [tuple(r) for r in golden["find_pairs_sorted"][str(limit)]]
     big = bp.find_pairs_multi_gpu(1 << 36, devices)
     assert [(p.m, p.n, p.kind) for p in big] == [(p.m, p.n, p.kind) for p in bp.find_pairs(1 << 36)]
+
+
+def _nccl_worker(port, limit, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_01099_b200.dist import find_pairs_distributed
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    assert dist.get_backend() == "nccl"
+    pairs = find_pairs_distributed(limit, device=0)  # item shard 0 of 1; rows gathered by NCCL on cuda:0
+    q.put([(int(p.kind), p.m, p.n, p.rad_m, p.rad_m_plus_1) for p in pairs])
+    dist.destroy_process_group()
+
+
+def test_nccl_row_gather_one_rank(golden):
+    """The NCCL code path of dist.py (two all_gather_into_tensor calls on the rank's GPU),
+    with the one rank this box has; every pair below 2^24 with its radicals."""
+    limit = 1 << 24
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), limit, q))
+    p.start()
+    got = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert got == [tuple(r) for r in golden["find_pairs_sorted"][str(limit)]]
