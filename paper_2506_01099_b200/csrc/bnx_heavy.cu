@@ -85,20 +85,35 @@ __device__ __forceinline__ uint64_t surplus_bound(uint64_t c, const HeavyArgs& a
 
 // The same for c < 2^32 in 32-bit arithmetic (narrow y: the 64-bit remainder and products
 // are most of the bound's cost).
+__device__ __forceinline__ float approx_rsqrt(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float approx_cbrt(float x) {  // x > 0: 2^(log2(x) / 3)
+    float l, r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (1.0f / 3.0f)));
+    return r;
+}
+// The roots here only have to land within 0.5 of the integer ones (c < 2^32: sqrt < 2^16,
+// cbrt < 1626, relative errors of the MUFU approximations ~1e-6), or be an upper bound with
+// the 1.0001 margin, so the hardware approximations replace the IEEE sqrtf / cbrtf.
 __device__ __forceinline__ uint64_t surplus_bound32(uint32_t c, const HeavyArgs& a) {
     if (c < a.p1sq) return 1;
     uint32_t u = 1;
     const float cf = (float)c;
     if ((c & 7) == 1) {
-        const uint32_t q = (uint32_t)rintf(sqrtf(cf));  // q < 2^16 (q = 2^16 wraps to 0 != c)
+        const uint32_t q = (uint32_t)rintf(cf * approx_rsqrt(cf));  // q < 2^16 (q = 2^16 wraps to 0 != c)
         if (q * q == c) u = q;
     }
     if (c >= a.p1cube) {
-        const uint32_t v = (uint32_t)(sqrtf(cf * a.inv_p1f) * 1.0001f) + 1;
+        const float t = cf * a.inv_p1f;
+        const uint32_t v = (uint32_t)(t * approx_rsqrt(t) * 1.0001f) + 1;
         if (v > u) u = v;
         const uint32_t m63 = c % 63u;
         if (!a.cube_filter || m63 == 1 || m63 == 8 || m63 == 55 || m63 == 62) {
-            const uint64_t r = (uint64_t)rintf(cbrtf(cf));
+            const uint64_t r = (uint64_t)rintf(approx_cbrt(cf));
             if (r * r * r == c && r * r > u) u = (uint32_t)(r * r);
         }
     }
