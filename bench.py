@@ -386,20 +386,25 @@ def run_ours(args) -> None:
     if rank == 0:
         e2e_cold = {}
         for name, bound, kk in (("2^32 first kind", S_HEADLINE, 1), ("1.4e12 both kinds", theorem1.COMPLETENESS_BOUND, 3)):
-            fresh = _native.Context(local)
-            try:
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                rows = fresh.search(bound, kk, None, 0)
-                t1 = time.perf_counter()
-            finally:
-                fresh.close()
-            want = theorem1.known_pairs(bound, kind=None if kk == 3 else kk)
-            e2e_cold[name] = {"wall_ms": 1e3 * (t1 - t0), "n_per_s": (bound - 1) / (t1 - t0),
-                              "pairs": int(len(rows)),
-                              "matches_theorem_1": sorted((int(r["m"]), int(r["n"])) for r in rows) == want}
-        e2e_cold["note"] = ("host wall clock around the first bnx_search of a new context (CUDA context already "
-                            "up): device prime tables, surplus-class table, graph capture, search, D2H")
+            walls, ok_cold, npairs = [], True, 0
+            for rep in range(2):  # rep 0 may grow the device memory pool; rep 1 reuses it
+                fresh = _native.Context(local)
+                try:
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    rows = fresh.search(bound, kk, None, 0)
+                    walls.append(1e3 * (time.perf_counter() - t0))
+                finally:
+                    fresh.close()
+                want = theorem1.known_pairs(bound, kind=None if kk == 3 else kk)
+                ok_cold &= sorted((int(r["m"]), int(r["n"])) for r in rows) == want
+                npairs = int(len(rows))
+            e2e_cold[name] = {"wall_ms": walls[0], "wall_ms_second_context": walls[1],
+                              "n_per_s": (bound - 1) / (walls[0] / 1e3), "pairs": npairs, "matches_theorem_1": ok_cold}
+        e2e_cold["note"] = ("host wall clock around the first bnx_search of a new library context (CUDA context "
+                            "already up): device prime tables, surplus-class table, graph capture, search, D2H; "
+                            "the first new context may grow the device memory pool (page mapping), the second "
+                            "reuses what the first freed")
 
     # ---- the same step with the byte-screen engine (visits every integer; identical rows)
     screen_engine = None

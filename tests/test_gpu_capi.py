@@ -191,13 +191,14 @@ def test_rows_beyond_the_read_back_prefix(prefix, golden):
                                                                       key=lambda r: (r[1], r[2]))
 
 
-def test_smallest_limits_with_a_caller_prime_list():
+def test_smallest_limits_with_a_caller_prime_list(golden):
     """limit 3 (isqrt = 1: the supplied list covers it with no primes at all) returns the
     reference's empty result instead of failing in the table build; 4 and 10 stay golden."""
     import paper_2506_01099_b200 as bp
 
-    assert bp.find_pairs_sorted(3, bp.primes_up_to(1)) == []
-    assert bp.find_pairs_sorted(4, bp.primes_up_to(2)) == []
+    rows = lambda ps: [[int(p.kind), p.m, p.n, p.rad_m, p.rad_m_plus_1] for p in ps]  # noqa: E731
+    assert bp.find_pairs_sorted(3, bp.primes_up_to(1)) == [] == golden["find_pairs_sorted"]["3"]
+    assert rows(bp.find_pairs_sorted(4, bp.primes_up_to(2))) == golden["find_pairs_sorted"]["4"]
     with pytest.raises(ValueError):  # isqrt(4) = 2 is not covered by the primes up to 1
         bp.find_pairs_sorted(4, bp.primes_up_to(1))
     assert [(int(p.kind), p.m, p.n) for p in bp.find_pairs_sorted(10, bp.primes_up_to(3))] == \
