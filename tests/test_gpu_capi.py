@@ -239,3 +239,21 @@ def test_table_search_chunk_refuses_oversized_tables():
     buf = (_native.PairRow * 4)()
     assert L.bnx_table_search_chunk(ctx.handle, 0, (1 << 30) + 2, 2**40, 0, 0, buf, 4,
                                     ctypes.byref(found)) == _native.BNX_ERR_INVALID
+
+
+def test_c_program_through_the_abi(tmp_path, golden):
+    """examples/search_c.c, compiled with gcc against include/benelux_b200.h and linked to the
+    library, prints the reference CLI's rows for every pair below 2^32."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = str(tmp_path / "search_c")
+    lib = os.path.join(ROOT, "paper_2506_01099_b200")
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "examples", "search_c.c"),
+                    "-L", lib, "-lbenelux_b200", f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    out = subprocess.run([exe, str(2**32)], capture_output=True, text=True, check=True).stdout
+    exp = golden["expected_pairs_up_to"]["4294967296"]
+    want = sorted(exp["first"] + exp["second"], key=lambda r: (r[1], r[2]))
+    assert out == "kind,m,n,rad_m,rad_m1\n" + "".join(",".join(map(str, r)) + "\n" for r in want)
