@@ -163,3 +163,23 @@ def test_gpu_brute_force_golden(golden):
     for lim, rows in golden["brute_force"].items():
         got = [[int(p.kind), p.m, p.n, p.rad_m, p.rad_m_plus_1] for p in bp.brute_force_pairs(int(lim))]
         assert got == rows
+
+
+@pytest.mark.gpu
+def test_paper_range_run_with_checkpoints(tmp_path):
+    """The paper's full range through the CLI's chunked run at the reference's default chunk
+    (2^27: 10,431 chunks, a checkpoint after each): the rows equal Theorem 1 (42 pairs), and a
+    resume from the finished checkpoint leaves the file unchanged."""
+    from oracle import theorem1
+
+    out, ck = tmp_path / "p.csv", tmp_path / "p.ck"
+    args = ["--limit", str(theorem1.COMPLETENESS_BOUND), "--algo", "chunked", "--chunk-size", str(2**27),
+            "--output", str(out), "--checkpoint", str(ck)]
+    r = run_cli(*args)
+    assert r.returncode == 0, r.stderr
+    want = theorem1.known_rows(theorem1.COMPLETENESS_BOUND)
+    assert cli.canonical_file(str(out), "csv") == cli.canonical_csv(want)
+    assert cli.Progress.load(str(ck)).next_chunk == 10431
+    before = out.read_bytes()
+    assert run_cli(*args, "--resume").returncode == 0
+    assert out.read_bytes() == before
