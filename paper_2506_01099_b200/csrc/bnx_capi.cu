@@ -193,6 +193,7 @@ struct bnx_ctx {
     int engine = 0;  // 0: heavy-side generator (default), 1: byte screen (BNX_ENGINE=screen)
     bool trace = false;         // BNX_TRACE=1 (see Trace)
     int stop_after = 0;         // profiling only (BNX_STOP_AFTER): run a prefix of the heavy pipeline
+    int publish_env = 1;        // BNX_PUBLISH=0: heavy searches read back with a copy node
     int table_lanes = 1;        // Algorithm 3: lanes per element (BNX_TABLE_LANES: 1 or 4; 4 measured slower)
     bool skip_readback = false; // profiling only (BNX_SKIP_READBACK): no D2H copy (results invalid)
     bool host_classes = false;  // BNX_HOST_CLASSES=1: the class table by the host DFS (tests)
@@ -218,6 +219,11 @@ struct bnx_ctx {
     bnx_pair_t* pairs_p = nullptr;
     size_t pairs_cap = 0;
     unsigned char* h_io = nullptr;
+    unsigned char* d_h_io = nullptr;  // h_io as the device sees it (mapped pinned memory)
+    bool publish = true;              // heavy engine: rows and flags written to h_io by the kernels
+    bool q_publish = false;           // ... for the enqueued search
+    bool stats_stale = false;         // counters not yet read back (bnx_ctx_stats fetches them)
+    uint64_t q_pairs_hint = 0;
     uint64_t pair_prefix = PAIR_PREFIX;  // rows read back with the counters (BNX_PAIR_PREFIX: tests)
     unsigned long long* h_sctr = nullptr;
     int* h_sflags = nullptr;
@@ -806,6 +812,17 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ta.pairs = c->pairs_p;
     ta.pair_cap = c->pairs_cap;
     ta.ctr = c->ctr_p;
+    // the kernels publish the rows and overflow flags into the mapped host block themselves
+    // (no read-back copy node at the end of the graph); the block is zeroed here first, so a
+    // row with m = 0 marks the end of the list
+    const bool publish = c->publish_env && !c->stop_after && !c->skip_readback;
+    if (publish) {
+        ta.host_pairs = reinterpret_cast<bnx_pair_t*>(c->d_h_io + IO_PAIRS);
+        ta.host_prefix = c->pair_prefix;
+        ta.host_flags = reinterpret_cast<int*>(c->d_h_io + IO_FLAGS);
+        ha.host_flags = ta.host_flags;
+        std::memset(c->h_io + IO_FLAGS, 0, IO_PAIRS - IO_FLAGS + sizeof(bnx_pair_t) * c->pair_prefix);
+    }
     // two phases (generator; tail + read-back), so the timing events sit between them
     auto record_gen = [&]() -> int {
         if (!ha.nent) {  // (otherwise k_heavy_count zeroes the counters and flags)
@@ -830,7 +847,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         launch_tail_light(ta, grid_for(c), c->stream, single);
         CK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
         CK(cudaGetLastError());
-        return read_back(c);
+        return publish ? BNX_OK : read_back(c);
     };
     if (!c->use_graphs || c->timing == 2) {
         if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
@@ -884,6 +901,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         }
     }
     c->q_valid = true;
+    c->q_publish = publish;
     c->q_first = n_first;
     c->q_last = n_last;
     c->q_kinds = kinds;
@@ -933,6 +951,7 @@ int enqueue_screen(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds
     if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
     TRY(read_back(c));
     c->q_valid = true;
+    c->q_publish = false;
     c->q_first = n_first;
     c->q_last = n_last;
     c->q_kinds = kinds;
@@ -948,6 +967,7 @@ int empty_search(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds) 
     CK(cudaMemsetAsync(c->ctr_p, 0, sizeof(unsigned long long) * CTR_N, c->stream));
     CK(cudaMemsetAsync(c->sflags_p, 0, sizeof(int) * 4, c->stream));
     TRY(read_back(c));
+    c->q_publish = false;
     if (c->timing) {
         CK(cudaEventRecord(c->ev[0], c->stream));
         CK(cudaEventRecord(c->ev[1], c->stream));
@@ -980,39 +1000,64 @@ int prepare(bnx_ctx* c, uint64_t max_x, const uint64_t* primes, size_t np, uint6
     return BNX_OK;
 }
 
-// Sync, grow-and-retry on any capacity overflow, copy the pair list out.
+// The search's counters into the host block (a published search has not copied them).
+int read_counters(bnx_ctx* c) {
+    CK(cudaMemcpyAsync(c->h_io + IO_CTR, c->io.p + IO_CTR, sizeof(unsigned long long) * CTR_N, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return BNX_OK;
+}
+
+void fill_stats(bnx_ctx* c) {
+    const unsigned long long* h = c->h_sctr;
+    c->stats.survivors = h[CTR_SURV];
+    c->stats.candidates = h[CTR_CAND];
+    c->stats.residue_checks = h[CTR_CHECKS];
+    c->stats.matches = h[CTR_MATCH];
+    c->stats.max_residue_checks = h[CTR_MAXCHK];
+    c->stats.pairs = h[CTR_PAIRS];
+    c->stats_stale = false;
+}
+
+// Sync, grow-and-retry on any capacity overflow, copy the pair list out.  A published heavy
+// search (q_publish) left its first rows and its overflow flags in the host block: without
+// an overflow the rows are read from there and the counters only on request (stats).
 int collect(bnx_ctx* c, std::vector<bnx_pair_t>& rows) {
     if (!c->q_valid) return fail(BNX_ERR_INVALID, "no search enqueued");
     for (int attempt = 0; attempt < 8; ++attempt) {
         CK(cudaStreamSynchronize(c->stream));
         if (c->h_sflags[0]) return fail(BNX_ERR_CUDA, "screen bucket overflow");
-        const unsigned long long* h = c->h_sctr;
-        bool again = false;
         if (c->h_sflags[1]) return fail(BNX_ERR_CUDA, "heavy generator: k outside its table");
-        if (c->engine == 0) {
-            if (h[CTR_SURV] > c->q1.cap) { TRY(c->q1.ensure(h[CTR_SURV] * 2)); again = true; }
-            if (h[CTR_LIGHT] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_LIGHT] * 2)); again = true; }
-        } else if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
-        if (h[CTR_HEAVY] > c->heavy.cap) { TRY(c->heavy.ensure(h[CTR_HEAVY] * 2)); again = true; }
-        if (h[CTR_PAIRS] > c->pairs_cap) { TRY(ensure_pairs(c, h[CTR_PAIRS] * 2)); again = true; }
-        if (again) {
-            TRY(enqueue(c, c->q_first, c->q_last, c->q_kinds));
-            continue;
-        }
-        const uint64_t np = h[CTR_PAIRS];
-        rows.resize(np);
-        if (np <= c->pair_prefix) {
-            if (np) std::memcpy(rows.data(), c->h_pairs, sizeof(bnx_pair_t) * np);
+        const bool published = c->q_publish;
+        if (published && !c->h_sflags[2] && !c->h_sflags[3]) {  // the common case: no copy at all
+            uint64_t np = 0;
+            while (np < c->pair_prefix && c->h_pairs[np].m) ++np;
+            rows.assign(c->h_pairs, c->h_pairs + np);
+            c->stats_stale = true;
         } else {
-            CK(cudaMemcpyAsync(rows.data(), c->pairs_p, sizeof(bnx_pair_t) * np, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
+            if (published) TRY(read_counters(c));
+            const unsigned long long* h = c->h_sctr;
+            bool again = false;
+            if (c->engine == 0) {
+                if (h[CTR_SURV] > c->q1.cap) { TRY(c->q1.ensure(h[CTR_SURV] * 2)); again = true; }
+                if (h[CTR_LIGHT] > c->cand.cap) { TRY(c->cand.ensure(h[CTR_LIGHT] * 2)); again = true; }
+            } else if (h[CTR_SURV] > c->surv.cap) { TRY(c->surv.ensure(h[CTR_SURV] * 2)); again = true; }
+            if (h[CTR_HEAVY] > c->heavy.cap) { TRY(c->heavy.ensure(h[CTR_HEAVY] * 2)); again = true; }
+            if (h[CTR_PAIRS] > c->pairs_cap) { TRY(ensure_pairs(c, h[CTR_PAIRS] * 2)); again = true; }
+            if (again) {
+                TRY(enqueue(c, c->q_first, c->q_last, c->q_kinds));
+                continue;
+            }
+            const uint64_t np = h[CTR_PAIRS];
+            rows.resize(np);
+            if (np <= c->pair_prefix) {
+                if (np) std::memcpy(rows.data(), c->h_pairs, sizeof(bnx_pair_t) * np);
+            } else {
+                CK(cudaMemcpyAsync(rows.data(), c->pairs_p, sizeof(bnx_pair_t) * np, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+            }
+            fill_stats(c);
         }
-        c->stats.survivors = h[CTR_SURV];
-        c->stats.candidates = h[CTR_CAND];
-        c->stats.residue_checks = h[CTR_CHECKS];
-        c->stats.matches = h[CTR_MATCH];
-        c->stats.max_residue_checks = h[CTR_MAXCHK];
-        c->stats.pairs = np;
         if (c->timing) {
             CK(cudaEventElapsedTime(&c->screen_ms, c->ev[0], c->ev[1]));
             CK(cudaEventElapsedTime(&c->pipeline_ms, c->ev[0], c->ev[2]));
@@ -1080,7 +1125,8 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
         uint64_t keep = ~0ull;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         CK(preload_device(device, c->stream));
-        CK(cudaMallocHost(&c->h_io, IO_PAIRS + sizeof(bnx_pair_t) * PAIR_PREFIX));
+        CK(cudaHostAlloc(&c->h_io, IO_PAIRS + sizeof(bnx_pair_t) * PAIR_PREFIX, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer((void**)&c->d_h_io, c->h_io, 0));
         c->h_sctr = reinterpret_cast<unsigned long long*>(c->h_io + IO_CTR);
         c->h_sflags = reinterpret_cast<int*>(c->h_io + IO_FLAGS);
         c->h_pairs = reinterpret_cast<bnx_pair_t*>(c->h_io + IO_PAIRS);
@@ -1093,6 +1139,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_SCREEN_SKIP")) c->screen_skip = std::atoi(env);
     if (const char* env = std::getenv("BNX_ENGINE")) c->engine = std::strcmp(env, "screen") == 0 ? 1 : 0;
     if (const char* env = std::getenv("BNX_STOP_AFTER")) c->stop_after = std::atoi(env);
+    if (const char* env = std::getenv("BNX_PUBLISH")) c->publish_env = std::atoi(env);
     if (const char* env = std::getenv("BNX_TABLE_LANES")) c->table_lanes = std::atoi(env) == 4 ? 4 : 1;
     if (const char* env = std::getenv("BNX_SKIP_READBACK")) c->skip_readback = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_TRACE")) c->trace = std::atoi(env) != 0;
@@ -1187,8 +1234,14 @@ int bnx_ctx_set_stream(bnx_ctx_t* c, void* stream) {
     return BNX_OK;
 }
 
-int bnx_ctx_stats(const bnx_ctx_t* c, bnx_stats_t* out) {
-    if (!c || !out) return fail(BNX_ERR_INVALID, "null argument");
+int bnx_ctx_stats(const bnx_ctx_t* cc, bnx_stats_t* out) {
+    if (!cc || !out) return fail(BNX_ERR_INVALID, "null argument");
+    bnx_ctx* c = const_cast<bnx_ctx*>(cc);  // (the counters of a published search are read lazily)
+    if (c->stats_stale) {
+        TRY(activate(c));
+        TRY(read_counters(c));
+        fill_stats(c);
+    }
     *out = c->stats;
     return BNX_OK;
 }
@@ -1386,6 +1439,10 @@ int bnx_search_enqueue(bnx_ctx_t* c, uint64_t n_first, uint64_t n_last, uint32_t
     if (n_first < 1 || n_last < n_first) return fail(BNX_ERR_INVALID, "empty search domain");
     c->rows_pending = false;  // a new search drops rows nobody collected
     c->pending.clear();
+    if (c->q_valid) {  // an uncollected search may still write the host block the next one reuses
+        TRY(activate(c));
+        CK(cudaStreamSynchronize(c->stream));
+    }
     if (c->screen_tab.gen != c->gen || c->screen_tab.max_x < n_last + 1)  // prepared for a large enough bound
         return fail(BNX_ERR_INVALID, "bnx_prepare must cover n_last + 1 first");
     TRY(activate(c));

@@ -318,6 +318,7 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
         if (pL && slot < a.q1_cap) a.q1[slot] = make_ulonglong2((x - 1) | (1ull << 63), it.radx);
         const unsigned long long s2 = slot + pL;
         if (pU && s2 < a.q1_cap) a.q1[s2] = make_ulonglong2(x, it.radx);
+        if (a.host_flags && slot + pL + pU > a.q1_cap) a.host_flags[2] = 1;
     }
 }
 
@@ -441,6 +442,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
                     }
                 } else {
                     a.flags[1] = 1;
+                    if (a.host_flags) a.host_flags[1] = 1;
                 }
             }
             __syncthreads();
@@ -589,7 +591,11 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         // 3. canonical k of the chunk
         for (int kk = tid; kk < kn; kk += blockDim.x) {
             const uint64_t k = k0 + (uint64_t)st * kk;
-            if (k >= a.nkinfo) { a.flags[1] = 1; continue; }
+            if (k >= a.nkinfo) {
+                a.flags[1] = 1;
+                if (a.host_flags) a.host_flags[1] = 1;
+                continue;
+            }
             bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
             if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
             if (canon) s_list[atomicAdd(&s_nl, 1)] = (uint32_t)kk;
@@ -658,9 +664,11 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
     if (total > a.tail_heavy) {
         const unsigned long long h = atomicAdd(&a.ctr[CTR_HEAVY], 1ull);
         if (h < a.heavy_cap) a.heavy[h] = c;
+        else if (a.host_flags) a.host_flags[2] = 1;
     } else {
         const unsigned long long slot = atomicAdd(&a.ctr[CTR_LIGHT], 1ull);
         if (slot < a.cand_cap) a.cand[slot] = c;
+        else if (a.host_flags) a.host_flags[2] = 1;
     }
 }
 

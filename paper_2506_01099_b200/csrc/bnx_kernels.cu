@@ -421,8 +421,14 @@ __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_be
             atomicAdd(&a.ctr[CTR_MATCH], 1ull);
             if ((a.kinds & (1u << (kind - 1))) && m >= 1 && m < c.n) {
                 const unsigned long long s = atomicAdd(&a.ctr[CTR_PAIRS], 1ull);
-                if (s < a.pair_cap)
-                    a.pairs[s] = kind == 1 ? bnx_pair_t{m, c.n, c.r0, c.r1, 1, 0} : bnx_pair_t{m, c.n, c.r1, c.r0, 2, 0};
+                const bnx_pair_t row =
+                    kind == 1 ? bnx_pair_t{m, c.n, c.r0, c.r1, 1, 0} : bnx_pair_t{m, c.n, c.r1, c.r0, 2, 0};
+                if (s < a.pair_cap) a.pairs[s] = row;
+                if (a.host_pairs) {
+                    if (s < a.host_prefix) a.host_pairs[s] = row;
+                    else a.host_flags[3] = 1;
+                    if (s >= a.pair_cap) a.host_flags[2] = 1;
+                }
             }
         }
     }

@@ -61,6 +61,12 @@ struct TailArgs {
     bnx_pair_t* pairs;
     uint64_t pair_cap;
     unsigned long long* ctr;
+    // heavy engine: the first host_prefix rows also go straight to mapped pinned host memory,
+    // and any overflow raises host_flags[2] (capacity) / [3] (more rows than the prefix), so
+    // the search needs no read-back copy; null for the byte screen
+    bnx_pair_t* host_pairs;
+    uint64_t host_prefix;
+    int* host_flags;
 };
 
 // Heavy-side generator (bnx_heavy.cu).
@@ -111,6 +117,7 @@ struct HeavyArgs {
     uint64_t tail_heavy;      // candidates with more residue-class members go to k_tail_heavy
     uint32_t run_mult;        // k_heavy_screen: fetched runs per CTA (from CTR_RUNS) after the first
     uint32_t run_first;       // k_heavy_screen: share of the items in the first (static) runs, /256
+    int* host_flags;          // mapped pinned host flags: [1] k outside its table, [2] a buffer overflowed
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
 void launch_pdiv32(const BnxPDiv* pdiv, uint64_t n, uint4* out, cudaStream_t st);
