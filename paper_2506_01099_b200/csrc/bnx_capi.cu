@@ -170,9 +170,25 @@ struct bnx_ctx {
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     // the heavy engine's search as a CUDA graph, re-captured whenever its parameters change
     bool use_graphs = true;
-    cudaGraph_t graph = nullptr, graph2 = nullptr;
-    cudaGraphExec_t graph_exec = nullptr, graph_exec2 = nullptr;
-    std::vector<unsigned char> graph_key;
+    // captured searches keyed by their parameters, least recently used evicted: alternating
+    // searches (shards of one search run one after another, a streaming run's batch shapes)
+    // replay their own graphs instead of re-capturing
+    struct GraphEntry {
+        std::vector<unsigned char> key;
+        cudaGraph_t g = nullptr, g2 = nullptr;
+        cudaGraphExec_t e = nullptr, e2 = nullptr;
+        uint64_t used = 0;
+        void destroy() {
+            if (e) cudaGraphExecDestroy(e);
+            if (e2) cudaGraphExecDestroy(e2);
+            if (g) cudaGraphDestroy(g);
+            if (g2) cudaGraphDestroy(g2);
+            e = e2 = nullptr;
+            g = g2 = nullptr;
+        }
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t graph_tick = 0;
     int num_sms = 148;
     int screen_blocks_per_sm = 1;
     int screen_v = 0;
@@ -866,37 +882,51 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
         const uint64_t extra[4] = {(uint64_t)(uintptr_t)c->stream, (uint64_t)grid,
                                    (uint64_t)(uintptr_t)h.scan_temp.p ^ (uint64_t)h.scan_bytes << 1, (uint64_t)single};
         std::memcpy(kp + sizeof(ha) + sizeof(ta), extra, sizeof(extra));
-        if (!c->graph_exec || (!single && !c->graph_exec2) || key != c->graph_key) {
-            for (auto* ge : {&c->graph_exec, &c->graph_exec2})
-                if (*ge) cudaGraphExecDestroy(*ge), *ge = nullptr;
-            for (auto* g : {&c->graph, &c->graph2})
-                if (*g) cudaGraphDestroy(*g), *g = nullptr;
-            c->graph_key.clear();
-            auto capture = [&](auto&& fn, cudaGraph_t* g, cudaGraphExec_t* ge) -> int {
+        bnx_ctx::GraphEntry* ge = nullptr;
+        for (auto& g : c->graphs)
+            if (g.key == key) ge = &g;
+        if (!ge) {
+            constexpr size_t MAX_GRAPHS = 8;
+            if (c->graphs.size() >= MAX_GRAPHS) {
+                auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                            [](const auto& x, const auto& y) { return x.used < y.used; });
+                lru->destroy();
+                c->graphs.erase(lru);
+            }
+            c->graphs.emplace_back();
+            ge = &c->graphs.back();
+            auto capture = [&](auto&& fn, cudaGraph_t* g, cudaGraphExec_t* ex) -> int {
                 CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
                 const int rc = fn();
                 const cudaError_t ec = cudaStreamEndCapture(c->stream, g);
                 if (rc != BNX_OK) return rc;
                 if (ec != cudaSuccess) return fail(BNX_ERR_CUDA, std::string("stream capture: ") + cudaGetErrorString(ec));
-                CK(cudaGraphInstantiate(ge, *g, 0));
+                CK(cudaGraphInstantiate(ex, *g, 0));
                 return BNX_OK;
             };
+            int rc;
             if (single) {
-                TRY(capture([&]() -> int { TRY(record_gen()); return record_tail(); }, &c->graph, &c->graph_exec));
+                rc = capture([&]() -> int { TRY(record_gen()); return record_tail(); }, &ge->g, &ge->e);
             } else {
-                TRY(capture(record_gen, &c->graph, &c->graph_exec));
-                TRY(capture(record_tail, &c->graph2, &c->graph_exec2));
+                rc = capture(record_gen, &ge->g, &ge->e);
+                if (rc == BNX_OK) rc = capture(record_tail, &ge->g2, &ge->e2);
             }
-            c->graph_key = key;
+            if (rc != BNX_OK) {
+                ge->destroy();
+                c->graphs.pop_back();
+                return rc;
+            }
+            ge->key = key;
             tr.mark("enqueue: graph capture");
         }
+        ge->used = ++c->graph_tick;
         if (single) {
-            CK(cudaGraphLaunch(c->graph_exec, c->stream));
+            CK(cudaGraphLaunch(ge->e, c->stream));
         } else {
             CK(cudaEventRecord(c->ev[0], c->stream));
-            CK(cudaGraphLaunch(c->graph_exec, c->stream));
+            CK(cudaGraphLaunch(ge->e, c->stream));
             CK(cudaEventRecord(c->ev[1], c->stream));
-            CK(cudaGraphLaunch(c->graph_exec2, c->stream));
+            CK(cudaGraphLaunch(ge->e2, c->stream));
             CK(cudaEventRecord(c->ev[2], c->stream));
         }
     }
@@ -1207,10 +1237,8 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     if (c->h_io) cudaFreeHost(c->h_io);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     g_alloc_stream = nullptr;
-    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
-    if (c->graph_exec2) cudaGraphExecDestroy(c->graph_exec2);
-    if (c->graph) cudaGraphDestroy(c->graph);
-    if (c->graph2) cudaGraphDestroy(c->graph2);
+    for (auto& g : c->graphs) g.destroy();
+    c->graphs.clear();
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     if (c->join_ev) cudaEventDestroy(c->join_ev);
