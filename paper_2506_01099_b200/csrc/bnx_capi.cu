@@ -890,6 +890,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
             if (c->graphs.size() >= MAX_GRAPHS) {
                 auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
                                             [](const auto& x, const auto& y) { return x.used < y.used; });
+                CK(cudaStreamSynchronize(c->stream));  // (no launch of the evicted graph may be pending)
                 lru->destroy();
                 c->graphs.erase(lru);
             }
