@@ -257,3 +257,14 @@ def test_c_program_through_the_abi(tmp_path, golden):
     exp = golden["expected_pairs_up_to"]["4294967296"]
     want = sorted(exp["first"] + exp["second"], key=lambda r: (r[1], r[2]))
     assert out == "kind,m,n,rad_m,rad_m1\n" + "".join(",".join(map(str, r)) + "\n" for r in want)
+
+
+def test_graph_cache_eviction_keeps_results():
+    """More distinct searches than the context's graph cache holds (8), twice over: every
+    replayed or re-captured graph returns the same rows as the first time."""
+    import paper_2506_01099_b200 as bp
+
+    domains = [(1 + 7 * i, 2**24 + 99991 * i) for i in range(11)]
+    first = [np.ascontiguousarray(bp.search.search_rows(lo, hi)).tobytes() for lo, hi in domains]
+    again = [np.ascontiguousarray(bp.search.search_rows(lo, hi)).tobytes() for lo, hi in reversed(domains)]
+    assert first == list(reversed(again))
