@@ -487,6 +487,7 @@ def run_ours(args) -> None:
         sieve = {"kernel": "k_sieve_exact", "integers": n_sieve, "ms": t_ms, "achieved": gbs, "peak": peak_hbm,
                  "unit": "GB/s", "frac": gbs / peak_hbm, "bound": "hbm",
                  "bytes_per_integer": 8, "check_rad_2^30": check,
+                 "slots": "32-bit shared-memory slots (window below 2^32), u64 output",
                  "write_only_peak_measured": write_peak, "frac_of_write_only_peak": gbs / write_peak}
         del out
         torch.cuda.empty_cache()

@@ -89,6 +89,7 @@ struct Tables {
     uint64_t max_x = 0;
     int include_two = -1;
     uint32_t tile = 0;
+    int nwarps = 0;
     uint64_t gen = ~0ull;
     DBuf<BnxProg> small, large;
     DBuf<BnxPDiv> pdiv;
@@ -195,6 +196,8 @@ struct bnx_ctx {
     int screen_skip = 0;  // profiling only
     int sieve_blocks_per_sm = 1;
     int sieve_v = 0;
+    int sieve_nv = 0;              // 32-bit-slot geometry for windows below 2^32 (BNX_SIEVE_NARROW; -1: off)
+    int sieve_narrow_blocks_per_sm = 1;
 
     // prime table (device u32 + host mirror)
     DBuf<uint32_t> primes;
@@ -218,6 +221,7 @@ struct bnx_ctx {
     int heavy_runs = -1;      // tuning only (BNX_HEAVY_RUNS, fetched screen runs per CTA); -1 = default
     int heavy_run_first = -1; // tuning only (BNX_HEAVY_RUN_FIRST, static share /256); -1 = default
     int heavy_kc = 0;         // tuning only (BNX_HEAVY_KC, k per sieve chunk, multiple of 8); 0 = default
+    int sieve_grid = 0;       // tuning only (BNX_SIEVE_GRID, k_heavy_sieve CTAs per SM); 0 = default
     uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
     DBuf<ulonglong2> q1;
@@ -454,7 +458,8 @@ std::vector<uint32_t> build_items(const std::vector<BnxProg>& small, uint32_t ti
 
 int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_t tile, int nwarps) {
     // a table built for a larger bound serves a smaller one: progressions q > x never divide x
-    if (t.gen == c->gen && t.max_x >= max_x && t.include_two == include_two && t.tile == tile) return BNX_OK;
+    if (t.gen == c->gen && t.max_x >= max_x && t.include_two == include_two && t.tile == tile && t.nwarps == nwarps)
+        return BNX_OK;
     const uint64_t root = isqrt_u64(max_x);
     const uint64_t np = (uint64_t)(std::upper_bound(c->h_primes.begin(), c->h_primes.end(), (uint32_t)std::min<uint64_t>(root, 0xFFFFFFFFull)) - c->h_primes.begin());
     const uint64_t cb = icbrt_u64(max_x);
@@ -516,6 +521,7 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
     t.max_x = max_x;
     t.include_two = include_two;
     t.tile = tile;
+    t.nwarps = nwarps;
     t.gen = c->gen;
     return BNX_OK;
 }
@@ -808,13 +814,15 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
     // (8 resident CTAs per SM at 32 registers) below ~2^33; more, smaller runs when the sieve
     // shares the GPU (40 per SM for domains of 2^38 or more: -2% at 2^40 and 2^44)
+    const bool wide_sieve = ha.kmin != ~0ull && !heavy_sieve_mask((int)np2);
     const int grid_mult = c->heavy_grid ? c->heavy_grid
-                                        : (ha.kmin == ~0ull ? 8 : (n_last - n_first >= (1ull << 38) ? 40 : 20));
+                                        : (!wide_sieve ? 8 : (n_last - n_first >= (1ull << 38) ? 40 : 20));
     const int grid = c->num_sms * grid_mult;
+    ha.sieve_ctas = c->sieve_grid ? (uint32_t)(c->num_sms * c->sieve_grid) : (wide_sieve ? 0u : (uint32_t)(c->num_sms * 4));
     // measured (scripts/sweep_env.sh BNX_HEAVY_RUNS / BNX_HEAVY_RUN_FIRST): in the one-wave
     // case, half the items in static runs and the rest in 2 fetched runs per CTA (-10% at
     // 2^32); with several waves (sieve bounds) the CTA scheduler already balances
-    ha.run_mult = c->heavy_runs >= 0 ? (uint32_t)c->heavy_runs : (ha.kmin == ~0ull ? 2u : 0u);
+    ha.run_mult = c->heavy_runs >= 0 ? (uint32_t)c->heavy_runs : (!wide_sieve ? 2u : 0u);
     ha.run_first = c->heavy_run_first >= 0 ? (uint32_t)c->heavy_run_first : 128u;
     TailArgs ta;
     std::memset(&ta, 0, sizeof(ta));
@@ -1180,6 +1188,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_HEAVY_RUNS")) c->heavy_runs = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_RUN_FIRST")) c->heavy_run_first = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_KC")) c->heavy_kc = std::max(0, std::atoi(env)) & ~7;
+    if (const char* env = std::getenv("BNX_SIEVE_GRID")) c->sieve_grid = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_PAIR_PREFIX"))
         c->pair_prefix = std::min<uint64_t>(PAIR_PREFIX, (uint64_t)std::max(0, std::atoi(env)));
     if (const char* env = std::getenv("BNX_TAIL_HEAVY")) c->tail_heavy = std::strtoull(env, nullptr, 10);
@@ -1202,7 +1211,17 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_blocks_per_sm, sv.fn, sv.threads, sv.smem));
     }
     c->screen_blocks_per_sm = std::max(1, c->screen_blocks_per_sm);
+    if (const char* env = std::getenv("BNX_SIEVE_NARROW")) {
+        const int v = std::atoi(env);
+        c->sieve_nv = (v >= 0 && v < sieve_narrow_count()) ? v : -1;
+    }
+    if (c->sieve_nv >= 0) {
+        const SieveVariant& sv = sieve_narrow(c->sieve_nv);
+        CK(cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sv.smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_narrow_blocks_per_sm, sv.fn, sv.threads, sv.smem));
+    }
     c->sieve_blocks_per_sm = std::max(1, c->sieve_blocks_per_sm);
+    c->sieve_narrow_blocks_per_sm = std::max(1, c->sieve_narrow_blocks_per_sm);
     *out = c;
     return BNX_OK;
 }
@@ -1361,7 +1380,10 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
     const uint64_t end = start + (length - 1);
     const uint64_t need = isqrt_u64(end);
     TRY(ensure_primes(c, primes, np, plimit, need));
-    const SieveVariant& sv = sieve_variant(c->sieve_v);
+    // every slot value is at most the window's end: 32-bit slots below 2^32
+    const bool narrow = c->sieve_nv >= 0 && end < (1ull << 32);
+    const SieveVariant& sv = narrow ? sieve_narrow(c->sieve_nv) : sieve_variant(c->sieve_v);
+    const int bps = narrow ? c->sieve_narrow_blocks_per_sm : c->sieve_blocks_per_sm;
     TRY(build_tables(c, c->sieve_tab, end, fast ? 0 : 1, (uint32_t)sv.tile, sv.threads / 32));
     if (c->sieve_tab.nsmall > (uint32_t)SIEVE_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     TRY(c->flags.ensure(4));
@@ -1376,7 +1398,7 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
         SieveArgs sa{start + off, len, c->sieve_tab.small.p, (int)c->sieve_tab.nsmall, c->sieve_tab.large.p,
                      c->sieve_tab.nlarge, c->sieve_tab.items.p, c->sieve_tab.nitems, fast, dst, c->flags.p};
         const uint64_t nseg = (len + SEG - 1) / SEG;
-        const int grid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * c->sieve_blocks_per_sm);
+        const int grid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * bps);
         sv.launch(sa, grid, c->stream);
         CK(cudaGetLastError());
         if (!out_dev) CK(cudaMemcpyAsync(out_host + off, dst, sizeof(uint64_t) * len, cudaMemcpyDeviceToHost, c->stream));

@@ -234,10 +234,13 @@ struct HeavyItem {
 // The y tests of one heavy x (both sides), see the file comment.  Shared tables per odd
 // prime <= P2: (p^-1 mod 2^64, floor((2^64-1)/p)), the same mod 2^32, p, and 2^32 mod p.
 // NARROW: both y below 2^32 -- every test, division and bound in 32-bit arithmetic (the
-// kernel is bound by its ALU/IMAD instruction count).
-template <bool NARROW>
+// kernel is bound by its ALU/IMAD instruction count).  SIEVED: the divisibility masks come
+// from k_heavy_sieve's progression marks (word w of the item at sm[w * stride]) instead of
+// the per-prime tests.
+template <bool NARROW, bool SIEVED = false>
 __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
-                                             const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32) {
+                                             const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32,
+                                             const uint32_t* sm = nullptr, int stride = 0) {
     using W = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     const uint64_t x = it.x;
     const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
@@ -255,7 +258,9 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
     for (int j0 = 0; j0 < a.np2; j0 += 32) {
         const int jn = min(32, a.np2 - j0);
         uint32_t m = 0;
-        if constexpr (NARROW) {
+        if constexpr (SIEVED) {
+            m = sm[(j0 >> 5) * stride];
+        } else if constexpr (NARROW) {
             // one multiply per prime for both sides: (x -+ 1) p^-1 = x p^-1 -+ p^-1 (mod 2^32)
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
@@ -484,17 +489,28 @@ __device__ __forceinline__ uint64_t mod_by_lim(uint64_t v, uint64_t p, uint64_t 
     return r;
 }
 
+// MASK (at most 64 primes <= P2, bounds up to ~2^33): the marks set one bit per prime in two
+// mask words per k (an odd prime divides at most one of x - 1, x + 1), and step 4 is the
+// screen's own post-pass (y_tests_impl<., true>) on those words, in 32-bit arithmetic when
+// the chunk's y are below 2^32.  Otherwise (up to 1023 primes): hit lists of prime indices
+// per (k, side), 64-bit.
+template <bool MASK>
 __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
-    const int np2 = a.np2, kc = a.kc;
-    uint16_t* hits = reinterpret_cast<uint16_t*>(sm_raw);                      // [2][kc][HEAVY_HITS]
-    uint32_t* hcnt = reinterpret_cast<uint32_t*>(hits + 2 * kc * HEAVY_HITS);  // [2][kc / 4] packed bytes
-    ulonglong2* s_il = reinterpret_cast<ulonglong2*>(hcnt + kc / 2);          // np2
-    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + np2);                   // np2
-    int32_t* s_off = reinterpret_cast<int32_t*>(s_p + np2);                    // 2 np2
+    const int np2 = a.np2, kc = a.kc, np2p = (np2 + 31) & ~31;
+    ulonglong2* s_il = reinterpret_cast<ulonglong2*>(sm_raw);                  // np2
+    uint2* s_pd32 = reinterpret_cast<uint2*>(s_il + np2);                      // MASK: np2p
+    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + (MASK ? np2p : 0));   // np2
+    uint32_t* s_c32 = s_p + np2;                                               // MASK: np2p
+    int32_t* s_off = reinterpret_cast<int32_t*>(s_c32 + (MASK ? np2p : 0));    // 2 np2
     uint32_t* s_kcm = reinterpret_cast<uint32_t*>(s_off + 2 * np2);            // np2: kc mod p
     uint32_t* s_task = s_kcm + np2;                                            // ntasks
     uint32_t* s_list = s_task + a.ntasks;                                      // kc
+    // MASK: mask word w of index kk at s_marks[w * kc + kk] (2 kc words); else packed byte
+    // counters [2][kc / 4] then the hit lists [2][kc][HEAVY_HITS]
+    uint32_t* s_marks = s_list + kc;
+    uint32_t* hcnt = s_marks;
+    uint16_t* hits = reinterpret_cast<uint16_t*>(s_marks + kc / 2);
     __shared__ BnxHeavyEnt s_e;
     __shared__ uint64_t s_k0, s_kend, s_cls_end, s_cls, s_kfirst;
     __shared__ int s_nl, s_fresh;
@@ -503,6 +519,17 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         s_il[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
         s_p[j] = (uint32_t)a.pdiv[j].p;
         s_kcm[j] = (uint32_t)kc % (uint32_t)a.pdiv[j].p;
+        if constexpr (MASK) {
+            const uint4 q = a.pd32[j];
+            s_pd32[j] = make_uint2(q.x, q.y);
+            s_c32[j] = q.w;
+        }
+    }
+    if constexpr (MASK) {
+        for (int j = np2 + tid; j < np2p; j += blockDim.x) {  // padding (its bits are masked off)
+            s_pd32[j] = make_uint2(1u, 0u);
+            s_c32[j] = 0u;
+        }
     }
     for (int t = tid; t < a.ntasks; t += blockDim.x) s_task[t] = a.tasks[t];
     if (a.nent == 0) return;
@@ -514,19 +541,9 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         if (tid < 32) {  // warp 0 finds the chunk's class
             const bool enter = ch == c_begin || ch >= s_cls_end;
             if (enter) {
-                uint64_t cls;
-                if (ch == c_begin) {  // first chunk of the run: first class with chunk prefix > ch
-                    cls = first_class_above_warp<true>(a.incl, a.nent, ch, tid);
-                } else {  // the next sieve class: the 32 lanes probe the following classes
-                    uint64_t from = s_cls + 1;
-                    for (;;) {
-                        const uint64_t j = from + tid;
-                        const bool hit = j < a.nent && (a.incl[j] >> 40) > ch;
-                        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-                        if (bal) { cls = from + __ffs(bal) - 1; break; }
-                        from += 32;
-                    }
-                }
+                // the class: first with chunk prefix > ch (a 32-way search: the sieved classes
+                // can be sparse among the trial classes, so no linear probe from the last one)
+                const uint64_t cls = first_class_above_warp<true>(a.incl, a.nent, ch, tid);
                 if (tid == 0) {
                     const uint64_t first = cls ? a.incl[cls - 1] >> 40 : 0;
                     s_e = a.ent[cls];
@@ -571,7 +588,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                 s_off[2 * j + 1] = (int32_t)(((uint32_t)s_off[2 * j + 1] + d) % p);
             }
         }
-        for (int w = tid; w < kc / 2; w += blockDim.x) hcnt[w] = 0;
+        for (int w = tid; w < (MASK ? 2 * kc : kc / 2); w += blockDim.x) s_marks[w] = 0;
         __syncthreads();
         // 2. marks: append j to the hit list of (k, side)
         for (int t = tid; t < a.ntasks; t += blockDim.x) {
@@ -582,10 +599,14 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
             if (off < 0) continue;
             const uint32_t p = s_p[j];
             for (uint32_t kk = (uint32_t)off + r * p; kk < (uint32_t)kn; kk += R * p) {
-                const uint32_t li = (uint32_t)side * kc + kk;
-                const uint32_t sh = 8 * (li & 3);
-                const uint32_t slot = (atomicAdd(&hcnt[li >> 2], 1u << sh) >> sh) & 0xFF;
-                if (slot < HEAVY_HITS) hits[li * HEAVY_HITS + slot] = (uint16_t)j;
+                if constexpr (MASK) {
+                    atomicOr(&s_marks[(j >> 5) * kc + kk], 1u << (j & 31));
+                } else {
+                    const uint32_t li = (uint32_t)side * kc + kk;
+                    const uint32_t sh = 8 * (li & 3);
+                    const uint32_t slot = (atomicAdd(&hcnt[li >> 2], 1u << sh) >> sh) & 0xFF;
+                    if (slot < HEAVY_HITS) hits[li * HEAVY_HITS + slot] = (uint16_t)j;
+                }
             }
         }
         // 3. canonical k of the chunk
@@ -604,6 +625,18 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         // 4. exact small factors of both sides, then the stage-1 test
         const int nl = s_nl;
         const uint64_t sigma = e.m * e.r;
+        if constexpr (MASK) {
+            const bool narrow = (k0 + (uint64_t)st * (uint64_t)(kn - 1)) * e.b + 1 < (1ull << 32);  // CTA-uniform
+            for (int li = tid; li < nl; li += blockDim.x) {
+                const uint32_t kk = s_list[li];
+                const uint64_t k = k0 + (uint64_t)st * kk;
+                const HeavyItem it{k * e.b, sigma, k * e.r};
+                if (narrow)
+                    y_tests_impl<true, true>(a, it, s_il, s_p, s_pd32, s_c32, s_marks + kk, kc);
+                else
+                    y_tests_impl<false, true>(a, it, s_il, s_p, s_pd32, s_c32, s_marks + kk, kc);
+            }
+        } else {
         for (int li = tid; li < nl; li += blockDim.x) {
             const uint32_t kk = s_list[li];
             const uint64_t k = k0 + (uint64_t)st * kk;
@@ -645,7 +678,9 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                 if (pL && slot < a.q1_cap) a.q1[slot] = make_ulonglong2((x - 1) | (1ull << 63), radx);
                 const unsigned long long s2 = slot + pL;
                 if (pU && s2 < a.q1_cap) a.q1[s2] = make_ulonglong2(x, radx);
+                if (a.host_flags && slot + pL + pU > a.q1_cap) a.host_flags[2] = 1;
             }
+        }
         }
     }
 }
@@ -801,16 +836,22 @@ __global__ void k_pdiv32(const BnxPDiv* __restrict__ pdiv, uint64_t n, uint4* __
     }
 }
 
+bool heavy_sieve_mask(int np2) { return np2 <= 64; }
+
 size_t heavy_sieve_smem(int np2, int kc, int ntasks) {
-    return sizeof(uint16_t) * (size_t)2 * kc * HEAVY_HITS + (size_t)2 * kc +
-           (sizeof(ulonglong2) + 2 * sizeof(uint32_t) + 2 * sizeof(int32_t)) * np2 +
-           sizeof(uint32_t) * ((size_t)ntasks + kc);
+    const size_t common = (sizeof(ulonglong2) + 2 * sizeof(uint32_t) + 2 * sizeof(int32_t)) * np2 +
+                          sizeof(uint32_t) * ((size_t)ntasks + kc);
+    if (heavy_sieve_mask(np2))  // + (inv32, lim32) and 2^32 mod p over np2p, 2 mask words per k
+        return common + (sizeof(uint2) + sizeof(uint32_t)) * (size_t)((np2 + 31) & ~31) + sizeof(uint32_t) * 2 * kc;
+    return common + sizeof(uint16_t) * (size_t)2 * kc * HEAVY_HITS + (size_t)2 * kc;
 }
 
 // Dynamic shared memory limits of the heavy kernels, set once per device (outside any
 // stream capture): the sieve's hit lists and the exact stage's prime table exceed 48 KB.
 cudaError_t heavy_configure() {
-    cudaError_t e = cudaFuncSetAttribute(k_heavy_sieve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_heavy_sieve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_heavy_sieve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
@@ -862,7 +903,11 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
             cudaEventRecord(ev_fork, st);
             cudaStreamWaitEvent(aux, ev_fork, 0);
             const size_t smemS = heavy_sieve_smem(a.np2, a.kc, a.ntasks);
-            k_heavy_sieve<<<grid, 256, smemS, aux>>>(a);
+            const int sgrid = a.sieve_ctas ? (int)a.sieve_ctas : grid;
+            if (heavy_sieve_mask(a.np2))
+                k_heavy_sieve<true><<<sgrid, 256, smemS, aux>>>(a);
+            else
+                k_heavy_sieve<false><<<sgrid, 256, smemS, aux>>>(a);
             cudaEventRecord(ev_join, aux);
         }
         const size_t np2p = (size_t)(a.np2 + 31) & ~(size_t)31;  // (see k_heavy_screen)

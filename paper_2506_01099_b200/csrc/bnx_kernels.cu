@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "bnx_kernels.cuh"
 #include "bnx_math.cuh"
 #include "bnx_rad.cuh"
@@ -517,11 +519,14 @@ __global__ void __launch_bounds__(256) k_tail_heavy(TailArgs a) {
 // start value x (or x with surplus twos stripped, _kernels.py:33-45), each hit of p^e
 // divides the slot by p exactly (multiply by p^-1 mod 2^64; shift for p = 2) through a
 // 64-bit shared CAS so concurrent progressions on one slot compose.
-__device__ __forceinline__ void div_slot(unsigned long long* s, uint64_t inv, bool two) {
-    unsigned long long old = *s, assumed;
+// (V = unsigned int: windows below 2^32, where every slot value fits 32 bits and p^-1 mod
+// 2^32 is the low half of p^-1 mod 2^64.)
+template <typename V>
+__device__ __forceinline__ void div_slot(V* s, uint64_t inv, bool two) {
+    V old = *s, assumed;
     do {
         assumed = old;
-        const unsigned long long nv = two ? (assumed >> 1) : assumed * inv;
+        const V nv = two ? (V)(assumed >> 1) : (V)(assumed * (V)inv);
         old = atomicCAS(s, assumed, nv);
     } while (old != assumed);
 }
@@ -545,14 +550,18 @@ __device__ __forceinline__ void bulk_wait_read() {  // the issuing thread's grou
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <int TILE, int NT, int THREADS, int BCAP, int MAXS, int MINB, bool ASYNC>
+// NARROW (windows ending below 2^32): 32-bit slots -- half the shared memory per tile, so
+// more CTAs per SM, and 32-bit CAS; the write-out widens each pair to the u64 output.
+template <int TILE, int NT, int THREADS, int BCAP, int MAXS, int MINB, bool ASYNC, bool NARROW = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
+    static_assert(!(ASYNC && NARROW), "the bulk write-out copies u64 slots");
+    using V = typename std::conditional<NARROW, unsigned int, unsigned long long>::type;
     constexpr int NW = THREADS / 32;
     constexpr uint64_t SEG = (uint64_t)TILE * NT;
     constexpr int NBUF = ASYNC ? 2 : 1;
     extern __shared__ __align__(16) unsigned long long sm64[];
-    unsigned long long* r0 = sm64;                       // NBUF * TILE slots
-    unsigned long long* bent = r0 + NBUF * TILE;         // NT * BCAP : (p << 16 | loc)
+    V* r0 = reinterpret_cast<V*>(sm64);                  // NBUF * TILE slots
+    unsigned long long* bent = sm64 + NBUF * TILE * sizeof(V) / 8;  // NT * BCAP : (p << 16 | loc)
     unsigned long long* s_inv = bent + NT * BCAP;        // MAXS
     uint32_t* bcnt = (uint32_t*)(s_inv + MAXS);          // NT
     uint32_t* s_q = bcnt + NT;                           // MAXS (sorted by q on the host)
@@ -595,7 +604,21 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
         // per thread and 16-byte stores: exactly one of them is even, and only that one can
         // need the shift.  Thread g always owns slots 2g, 2g+1 (init, write-out), so the
         // write-out of tile t and the init of tile t+1 share one pass with no barrier.
-        auto init_pair = [&](unsigned long long* buf, uint64_t tile0, int g) {
+        auto init_pair = [&](V* buf, uint64_t tile0, int g) {
+            if constexpr (NARROW) {  // 32-bit and branch-free: the even one is x0 + (x0 odd), and
+                // xe >> (ctz(xe) - 1) leaves xe = 2 (mod 4) unchanged (xe = 0 only past the window's end)
+                const uint32_t x0 = (uint32_t)tile0 + 2u * (uint32_t)g;
+                uint32_t v0 = x0, v1 = x0 + 1u;
+                if (a.fast) {
+                    const uint32_t odd0 = x0 & 1u;
+                    const uint32_t xe = x0 + odd0;
+                    const uint32_t ve = xe ? xe >> (__ffs(xe) - 2) : 0u;
+                    v0 = odd0 ? v0 : ve;
+                    v1 = odd0 ? ve : v1;
+                }
+                reinterpret_cast<uint2*>(buf)[g] = make_uint2(v0, v1);
+                return;
+            }
             const uint64_t x0 = tile0 + 2u * (uint32_t)g;
             uint64_t v0 = x0, v1 = x0 + 1;
             if (a.fast) {
@@ -614,7 +637,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
         for (int t = 0; t < NT; ++t) {
             const uint64_t toff = seg_off + (uint64_t)t * TILE;
             if (toff >= a.length) break;
-            unsigned long long* r = r0 + cur * TILE;
+            V* r = r0 + cur * TILE;
             __syncthreads();
             // per-tile progressions: balanced work items (see k_screen), exact division per hit
             const int it_end = (int)s_item[warp + 1];
@@ -656,7 +679,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
             uint64_t* dst = a.out + toff;
             const bool next = t + 1 < NT && toff + TILE < a.length;
             const bool whole = lim == TILE && ((((uintptr_t)dst) & 15) == 0);
-            if (ASYNC) {
+            if constexpr (ASYNC) {
                 unsigned long long* rn = r0 + (cur ^ 1) * TILE;
                 if (whole) {
                     if (tid == 0) {
@@ -680,7 +703,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
                 // write out (16-byte streaming stores; the values are not re-read on the device)
                 // fused with the next tile's init
                 for (int g = tid; g < TILE / 2; g += THREADS) {
-                    __stcs(reinterpret_cast<ulonglong2*>(dst) + g, reinterpret_cast<const ulonglong2*>(r)[g]);
+                    if constexpr (NARROW) {
+                        const uint2 v = reinterpret_cast<const uint2*>(r)[g];
+                        __stcs(reinterpret_cast<ulonglong2*>(dst) + g, make_ulonglong2(v.x, v.y));
+                    } else {
+                        __stcs(reinterpret_cast<ulonglong2*>(dst) + g, reinterpret_cast<const ulonglong2*>(r)[g]);
+                    }
                     if (next) init_pair(r, a.start + toff + TILE, g);
                 }
             } else {  // ragged last tile or an output only 8-byte aligned: same slot ownership
@@ -1114,15 +1142,15 @@ __global__ void __launch_bounds__(256) k_table_quad(TableArgs a) {
 
 // ------------------------------------------------------------------------------------
 // Launch helpers (instantiations and dynamic shared memory sizes).
-template <int TILE, int NT, int BCAP, bool ASYNC = false>
+template <int TILE, int NT, int BCAP, bool ASYNC = false, bool NARROW = false>
 constexpr size_t sieve_smem() {
-    return sizeof(unsigned long long) * ((size_t)TILE * (ASYNC ? 2 : 1) + (size_t)NT * BCAP + SIEVE_MAXS) +
-           sizeof(uint32_t) * ((size_t)NT + 5 * SIEVE_MAXS);
+    return (NARROW ? sizeof(uint32_t) : sizeof(unsigned long long)) * (size_t)TILE * (ASYNC ? 2 : 1) +
+           sizeof(unsigned long long) * ((size_t)NT * BCAP + SIEVE_MAXS) + sizeof(uint32_t) * ((size_t)NT + 5 * SIEVE_MAXS);
 }
-template <int TILE, int NT, int THREADS, int BCAP, int MINB, bool ASYNC>
+template <int TILE, int NT, int THREADS, int BCAP, int MINB, bool ASYNC, bool NARROW = false>
 void launch_sieve_v(const SieveArgs& a, int grid, cudaStream_t st) {
-    k_sieve_exact<TILE, NT, THREADS, BCAP, SIEVE_MAXS, MINB, ASYNC>
-        <<<grid, THREADS, sieve_smem<TILE, NT, BCAP, ASYNC>(), st>>>(a);
+    k_sieve_exact<TILE, NT, THREADS, BCAP, SIEVE_MAXS, MINB, ASYNC, NARROW>
+        <<<grid, THREADS, sieve_smem<TILE, NT, BCAP, ASYNC, NARROW>(), st>>>(a);
 }
 template <int TILE, int NT, int NWC, int BCAP>
 void launch_sieve_pipe(const SieveArgs& a, int grid, cudaStream_t st) {
@@ -1151,6 +1179,22 @@ static const SieveVariant kSieveVariants[] = {
 };
 int sieve_variant_count() { return (int)(sizeof(kSieveVariants) / sizeof(kSieveVariants[0])); }
 const SieveVariant& sieve_variant(int i) { return kSieveVariants[i]; }
+// 32-bit-slot geometries for windows ending below 2^32 (BNX_SIEVE_NARROW, default 0; -1: off).
+// Measured on [1, 2^30] (scripts/sieve_variants.py, profiles/r02_sieve_narrow.jsonl): 1.40 ms
+// for the default against 2.17 ms for the u64 kernel; 1.43, 1.54, 1.63 ms for the others.
+// Half-size slots fit four CTAs per SM, and CTAs of 12 warps wait less at the per-tile
+// barriers than CTAs of 16 (512 threads: 1.54 ms) or 32 (1024: 2.30 ms).
+#define BNX_SIEVE_NARROW_VARIANT(T, N, H, B, M)                                                                        \
+    SieveVariant{T, N, H, B, (const void*)k_sieve_exact<T, N, H, B, SIEVE_MAXS, M, false, true>,                    \
+                 sieve_smem<T, N, B, false, true>(), launch_sieve_v<T, N, H, B, M, false, true>}
+static const SieveVariant kSieveNarrow[] = {
+    BNX_SIEVE_NARROW_VARIANT(8192, 32, 384, 64, 4),
+    BNX_SIEVE_NARROW_VARIANT(8192, 16, 256, 64, 5),
+    BNX_SIEVE_NARROW_VARIANT(8192, 32, 512, 64, 4),
+    BNX_SIEVE_NARROW_VARIANT(8192, 64, 512, 64, 3),
+};
+int sieve_narrow_count() { return (int)(sizeof(kSieveNarrow) / sizeof(kSieveNarrow[0])); }
+const SieveVariant& sieve_narrow(int i) { return kSieveNarrow[i]; }
 
 template <int TILE, int NT, int THREADS, int BCAP>
 constexpr size_t screen_smem() {
@@ -1241,7 +1285,7 @@ void launch_trial_division(uint64_t start, uint64_t length, const BnxPDiv* pd, u
 cudaError_t kernels_preload() {
     const void* fns[] = {(const void*)k_base_primes, (const void*)k_prime_seg, (const void*)k_scan_counts,
                          (const void*)k_narrow_primes, (const void*)k_build_tables, (const void*)k_tail,
-                         (const void*)k_tail_heavy, kSieveVariants[0].fn, kScreenVariants[0].fn};
+                         (const void*)k_tail_heavy, kSieveVariants[0].fn, kSieveNarrow[0].fn, kScreenVariants[0].fn};
     for (const void* f : fns) {
         cudaFuncAttributes at;
         const cudaError_t e = cudaFuncGetAttributes(&at, f);

@@ -118,10 +118,12 @@ struct HeavyArgs {
     uint32_t run_mult;        // k_heavy_screen: fetched runs per CTA (from CTR_RUNS) after the first
     uint32_t run_first;       // k_heavy_screen: share of the items in the first (static) runs, /256
     int* host_flags;          // mapped pinned host flags: [1] k outside its table, [2] a buffer overflowed
+    uint32_t sieve_ctas;      // k_heavy_sieve grid (0: the screen's)
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
 void launch_pdiv32(const BnxPDiv* pdiv, uint64_t n, uint4* out, cudaStream_t st);
 cudaError_t heavy_configure();
+bool heavy_sieve_mask(int np2);  // k_heavy_sieve marks bit masks (else hit lists)
 size_t heavy_sieve_smem(int np2, int kc, int ntasks);
 void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, int grid, cudaStream_t st,
                   cudaEvent_t ev_generated, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join,
@@ -202,6 +204,8 @@ struct SieveVariant {
 };
 int sieve_variant_count();
 const SieveVariant& sieve_variant(int i);
+int sieve_narrow_count();  // the same kernel with 32-bit slots (windows ending below 2^32)
+const SieveVariant& sieve_narrow(int i);
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st);
 void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st, bool pdl = false);  // heavy engine: k_tail only
 void launch_tail_heavy(const TailArgs& a, cudaStream_t st);            // heavy engine: k_tail_heavy only

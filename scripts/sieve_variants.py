@@ -1,7 +1,8 @@
 """A/B of the exact radical sieve geometries (BNX_SIEVE_VARIANT): for each compiled variant,
 in its own process, time k_sieve_exact over [1, 2^30] (min of 5, CUDA events, L2 flushed)
 and hash the output plus two windows high in the range, so the variants can be compared
-for speed and for identical radicals.  Prints one JSON line per variant."""
+for speed and for identical radicals.  Prints one JSON line per variant.  [1, 2^30] runs the
+32-bit-slot geometry BNX_SIEVE_NARROW (default 0; -1: the u64 variant itself)."""
 import hashlib
 import json
 import os
@@ -46,7 +47,8 @@ def child() -> None:
         torch.cuda.synchronize()
         hi.append(hashlib.sha256(out[1:m + 1].cpu().numpy().tobytes()).hexdigest()[:16])
     ms = min(times)
-    print(json.dumps({"variant": os.environ.get("BNX_SIEVE_VARIANT", "0"), "ms": ms,
+    print(json.dumps({"variant": os.environ.get("BNX_SIEVE_VARIANT", "0"),
+                      "narrow": os.environ.get("BNX_SIEVE_NARROW", "0"), "ms": ms,
                       "GBps": 8 * n / (ms / 1e3) / 1e9, "times": times, "sha_2p30": h, "sha_high": hi}))
 
 

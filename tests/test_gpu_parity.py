@@ -75,6 +75,29 @@ def test_sieve_large_window_vs_trial_division(orc):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("variant", ["-1", "0", "1", "2"])
+def test_sieve_narrow_slots_vs_oracle(orc, monkeypatch, variant):
+    """Windows ending below 2^32 run the sieve with 32-bit shared-memory slots (BNX_SIEVE_NARROW
+    picks the geometry, -1 the u64 kernel): windows at 1, ragged lengths, windows ending at
+    2^32 - 1 and one crossing 2^32 (u64 slots), both ctz modes, against the oracle's sieve."""
+    from paper_2506_01099_b200 import _native
+
+    monkeypatch.setenv("BNX_SIEVE_NARROW", variant)
+    ctx = _native.Context(0)
+    try:
+        rng = np.random.default_rng(int(variant) + 7)
+        cases = [(1, 3 * 2**20 + 5), (2**32 - 2**21, 2**21), (2**32 - 1, 1), (2**32 - 2**20 + 3, 2**20 + 9)]
+        cases += [(int(rng.integers(1, 2**32 - 2**20)), int(rng.integers(1, 2**20))) for _ in range(6)]
+        for start, length in cases:
+            for fast in (True, False):
+                need = math.isqrt(start + length - 1)
+                got = ctx.sieve_radicals(start, length, None, 0, fast)
+                want = orc.sieve_segment(start, length, orc.primes_up_to(need + 1), fast)
+                assert np.array_equal(got, want), (variant, start, length, fast)
+    finally:
+        ctx.close()
+
+
 # ---------------------------------------------------------------- trial division ---------
 def test_trial_division_vectors(golden):
     for rec in golden["trial_division"]:
@@ -397,3 +420,29 @@ def test_item_shards_strong_config_partition():
     finally:
         ctx.set_shard(0, 1)
     assert sorted(parts) == full and len(full) == 20
+
+
+@pytest.mark.parametrize("kmin", [1, 64, 256])
+def test_sieve_mask_mode_at_small_bounds(orc, monkeypatch, kmin):
+    """k_heavy_sieve's mask mode (at most 64 primes below P2: bounds up to ~2^33) forced onto
+    every class with >= kmin k (BNX_HEAVY_KMIN, read when a context is created): exact
+    candidate counts against the oracle's sieve, the same rows as the default split, on
+    domains with 32-bit and wider y, and the 2^32 search's survivor list is unchanged."""
+    from paper_2506_01099_b200 import _native
+
+    base = _native.context(0)
+    monkeypatch.setenv("BNX_HEAVY_KMIN", str(kmin))
+    ctx = _native.Context(0)
+    try:
+        for lo, hi in [(1, 2**22), (2**32 - 2**21, 2**32 + 2**21), (2**33 - 2**20, 2**33), (5, 5)]:
+            got = ctx.search_domain(lo, hi, 3, None, 0)
+            assert ctx.stats()["candidates"] == exact_candidates(orc, lo, hi), (kmin, lo, hi)
+            want = base.search_domain(lo, hi, 3, None, 0)
+            assert got.tobytes() == want.tobytes(), (kmin, lo, hi)
+        got = ctx.search(2**32, 3, None, 0)
+        st = ctx.stats()
+        want = base.search(2**32, 3, None, 0)
+        assert got.tobytes() == want.tobytes()
+        assert st["survivors"] == base.stats()["survivors"] and st["candidates"] == 2253
+    finally:
+        ctx.close()
