@@ -222,9 +222,10 @@ struct bnx_ctx {
     int heavy_run_first = -1; // tuning only (BNX_HEAVY_RUN_FIRST, static share /256); -1 = default
     int heavy_kc = 0;         // tuning only (BNX_HEAVY_KC, k per sieve chunk, multiple of 8); 0 = default
     int sieve_grid = 0;       // tuning only (BNX_SIEVE_GRID, k_heavy_sieve CTAs per SM); 0 = default
+    int exact_warp = -1;      // tuning only (BNX_EXACT_WARP: 1 warp / 0 thread per survivor); -1 = by bound
     uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
-    DBuf<ulonglong2> q1;
+    DBuf<BnxSurv> q1;
     DBuf<BnxCand> cand;
 
     DBuf<uint64_t> surv;
@@ -818,6 +819,10 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     const int grid_mult = c->heavy_grid ? c->heavy_grid
                                         : (!wide_sieve ? 8 : (n_last - n_first >= (1ull << 38) ? 40 : 20));
     const int grid = c->num_sms * grid_mult;
+    // k_heavy_exact: a thread per survivor from P2 on (measured: 0.45 ms at 2^40 against
+    // 1.17 ms for a warp per survivor trying only the deciding primes, whose per-survivor set-up
+    // outweighs the primes it skips); the warp form serves domains with few survivors
+    ha.exact_warp = c->exact_warp >= 0 ? c->exact_warp : 0;
     ha.sieve_ctas = c->sieve_grid ? (uint32_t)(c->num_sms * c->sieve_grid) : (wide_sieve ? 0u : (uint32_t)(c->num_sms * 4));
     // measured (scripts/sweep_env.sh BNX_HEAVY_RUNS / BNX_HEAVY_RUN_FIRST): in the one-wave
     // case, half the items in static runs and the rest in 2 fetched runs per CTA (-10% at
@@ -1189,6 +1194,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_HEAVY_RUN_FIRST")) c->heavy_run_first = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_HEAVY_KC")) c->heavy_kc = std::max(0, std::atoi(env)) & ~7;
     if (const char* env = std::getenv("BNX_SIEVE_GRID")) c->sieve_grid = std::max(0, std::atoi(env));
+    if (const char* env = std::getenv("BNX_EXACT_WARP")) c->exact_warp = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_PAIR_PREFIX"))
         c->pair_prefix = std::min<uint64_t>(PAIR_PREFIX, (uint64_t)std::max(0, std::atoi(env)));
     if (const char* env = std::getenv("BNX_TAIL_HEAVY")) c->tail_heavy = std::strtoull(env, nullptr, 10);

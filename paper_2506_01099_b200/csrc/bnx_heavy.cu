@@ -249,6 +249,7 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
     const int tL = __ffsll((long long)yL) - 1, tU = __ffsll((long long)yU) - 1;
     W cL = (W)(yL >> tL), cU = (W)(yU >> tU);
     W sL = tL ? (W)1 << (tL - 1) : (W)1, sU = tU ? (W)1 << (tU - 1) : (W)1;
+    W rL = tL ? (W)2 : (W)1, rU = tU ? (W)2 : (W)1;  // radicals of the divided-off parts
     const uint32_t x32 = (uint32_t)x, xh = (uint32_t)(x >> 32);
     // Divisibility by 32 primes at a time into a bit mask, branch-free (the lanes of a warp
     // stay converged): one bit per prime for both sides (an odd p divides at most one of
@@ -301,9 +302,11 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
             W t = cL * inv;
             if (vL && t <= lim) {  // p | cL exactly (rejects a wrapped false bit)
                 cL = t;
+                rL *= pp;
                 for (t = cL * inv; t <= lim; t = cL * inv) { cL = t; sL *= pp; }
             } else if ((t = cU * inv) <= lim) {
                 cU = t;
+                rU *= pp;
                 for (t = cU * inv; t <= lim; t = cU * inv) { cU = t; sU *= pp; }
             }
         }
@@ -320,9 +323,9 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
     const bool pU = vU && twice_prod_ge(it.sigma, (uint64_t)sU * uU, x + 1);
     if (pL || pU) {
         const unsigned long long slot = atomicAdd(&a.ctr[CTR_SURV], (unsigned long long)(pL + pU));
-        if (pL && slot < a.q1_cap) a.q1[slot] = make_ulonglong2((x - 1) | (1ull << 63), it.radx);
+        if (pL && slot < a.q1_cap) a.q1[slot] = BnxSurv{(x - 1) | (1ull << 63), it.radx, (uint64_t)cL, (uint64_t)rL};
         const unsigned long long s2 = slot + pL;
-        if (pU && s2 < a.q1_cap) a.q1[s2] = make_ulonglong2(x, it.radx);
+        if (pU && s2 < a.q1_cap) a.q1[s2] = BnxSurv{x, it.radx, (uint64_t)cU, (uint64_t)rU};
         if (a.host_flags && slot + pL + pU > a.q1_cap) a.host_flags[2] = 1;
     }
 }
@@ -644,13 +647,14 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
             const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
             const bool vU = x >= a.n_first && x <= a.n_last;
             bool pL = false, pU = false;
+            uint64_t cs[2] = {1, 1}, rs[2] = {1, 1};  // cofactor and radical of the divided-off part
 #pragma unroll
             for (int side = 0; side < 2; ++side) {
                 const bool valid = side ? vL : vU;
                 if (!valid) continue;
                 const uint64_t y = side ? x - 1 : x + 1;
                 const int tz = __ffsll((long long)y) - 1;
-                uint64_t c = y >> tz, sy = tz ? 1ull << (tz - 1) : 1ull;
+                uint64_t c = y >> tz, sy = tz ? 1ull << (tz - 1) : 1ull, ry = tz ? 2 : 1;
                 const uint32_t hl = (uint32_t)side * kc + kk;
                 const uint32_t nh = (hcnt[hl >> 2] >> (8 * (hl & 3))) & 0xFF;
                 if (nh <= (uint32_t)HEAVY_HITS) {
@@ -658,6 +662,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                         const int j = hits[hl * HEAVY_HITS + h];
                         const ulonglong2 d = s_il[j];
                         c *= d.x;
+                        ry *= s_p[j];
                         while (c * d.x <= d.y) { c *= d.x; sy *= s_p[j]; }
                     }
                 } else {  // more distinct small primes than slots (rare): trial division
@@ -665,19 +670,22 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                         const ulonglong2 d = s_il[j];
                         if (c * d.x <= d.y) {
                             c *= d.x;
+                            ry *= s_p[j];
                             while (c * d.x <= d.y) { c *= d.x; sy *= s_p[j]; }
                         }
                     }
                 }
                 const bool pass = twice_prod_ge(sigma, sy * surplus_bound(c, a), side ? x : x + 1);
                 if (side) pL = pass; else pU = pass;
+                cs[side] = c;
+                rs[side] = ry;
             }
             if (pL || pU) {
                 const uint64_t radx = k * e.r;
                 const unsigned long long slot = atomicAdd(&a.ctr[CTR_SURV], (unsigned long long)(pL + pU));
-                if (pL && slot < a.q1_cap) a.q1[slot] = make_ulonglong2((x - 1) | (1ull << 63), radx);
+                if (pL && slot < a.q1_cap) a.q1[slot] = BnxSurv{(x - 1) | (1ull << 63), radx, cs[1], rs[1]};
                 const unsigned long long s2 = slot + pL;
-                if (pU && s2 < a.q1_cap) a.q1[s2] = make_ulonglong2(x, radx);
+                if (pU && s2 < a.q1_cap) a.q1[s2] = BnxSurv{x, radx, cs[0], rs[0]};
                 if (a.host_flags && slot + pL + pU > a.q1_cap) a.host_flags[2] = 1;
             }
         }
@@ -707,20 +715,22 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
     }
 }
 
-// Exact radical of the other side (one thread per survivor: the odd primes <= cbrt(y_max)
-// from shared memory, 32 per bit mask as in y_tests; the cofactor is then 1, p, p^2 or pq),
-// the exact test R <= 2n, de-duplication, emission.
-// rad(o) of an odd o < 2^53 by one thread: trial division by the odd primes <= cbrt(y_max)
-// (32 at a time into a bit mask, unrolled with constant bit positions over the table padded
-// to a multiple of 32), then at most two primes remain (p, p^2 or pq).  NARROW: o < 2^32,
-// everything in 32-bit arithmetic.
+// Exact radical of the other side.  The survivor record carries y's cofactor c after the
+// odd primes <= P2 (every prime factor of c exceeds P2, so c has at most three) and the
+// radical `base` of the part divided off, so rad y = base * rad(c) and only the primes in
+// (P2, cbrt c] can still matter.
+//
+// rad(c) of such a c by one thread: trial division by the odd primes from P2 up to
+// cbrt(y_max) (32 at a time into a bit mask, unrolled with constant bit positions over the
+// table padded to a multiple of 32), then at most two primes remain (p, p^2 or pq).
+// NARROW: c < 2^32, everything in 32-bit arithmetic.
 template <bool NARROW>
-__device__ __forceinline__ uint64_t rad_odd_thread(uint64_t o, int np3, const ulonglong2* s_il3, const uint2* s_pd3,
-                                                   const uint32_t* s_p3, const uint32_t* s_c3) {
+__device__ __forceinline__ uint64_t rad_cofactor_thread(uint64_t o, int j_first, int np3, const ulonglong2* s_il3,
+                                                        const uint2* s_pd3, const uint32_t* s_p3, const uint32_t* s_c3) {
     using W = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     W c = (W)o, rad = 1;
     const uint32_t ol = (uint32_t)o, oh = (uint32_t)(o >> 32);
-    for (int j0 = 0; j0 < np3; j0 += 32) {
+    for (int j0 = j_first; j0 < np3; j0 += 32) {
         const int jn = min(32, np3 - j0);
         uint32_t m = 0;
         if constexpr (NARROW) {
@@ -764,6 +774,110 @@ __device__ __forceinline__ uint64_t rad_odd_thread(uint64_t o, int np3, const ul
     return r;
 }
 
+// First index i in [0, n) with sp[i] >= v (n if none), by the whole warp (warp-uniform v): 32
+// probes per round narrow [lo, hi] 32-fold.
+__device__ __forceinline__ int lower_bound_warp(const uint32_t* sp, int n, uint64_t v, int lane) {
+    int lo = 0, hi = n;  // the answer lies in [lo, hi]
+    while (hi - lo > 31) {
+        const int span = hi - lo;
+        const int q = lo + (int)((int64_t)span * (lane + 1) / 32);  // lane 31 probes hi
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, q >= n || sp[q] >= v);
+        const int j = __ffs(bal) - 1;
+        const int nlo = j ? lo + (int)((int64_t)span * j / 32) + 1 : lo;
+        hi = lo + (int)((int64_t)span * (j + 1) / 32);
+        lo = nlo;
+    }
+    const int q = lo + lane;
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, q >= hi || sp[q] >= v);
+    return lo + __ffs(bal) - 1;
+}
+
+// Index of a prime in [i0, i1) dividing c (the first such block of 32, lowest lane), or -1:
+// the warp tests 32 primes per step.
+__device__ __forceinline__ int divisor_in_warp(uint64_t c, int i0, int i1, const ulonglong2* s_il3, const uint2* s_pd3,
+                                               int lane) {
+    const bool narrow = c < (1ull << 32);
+    for (int b = i0; b < i1; b += 32) {
+        const int j = b + lane;
+        bool hit = false;
+        if (j < i1) {
+            if (narrow) {
+                const uint2 d = s_pd3[j];
+                hit = (uint32_t)c * d.x <= d.y;
+            } else {
+                const ulonglong2 d = s_il3[j];
+                hit = c * d.x <= d.y;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, hit);
+        if (bal) return b + __ffs(bal) - 1;
+    }
+    return -1;
+}
+
+// rad(c) from one prime divisor d = p_j of c (c has at most three prime factors, none of
+// them a repeated d unless d^2 | c): d^2 | c -> c = d^2 q, rad = d q; else c / d is p^2
+// (rad = d p) or squarefree (rad = c).
+__device__ __forceinline__ uint64_t rad_from_divisor(uint64_t c, int j, const ulonglong2* s_il3, const uint32_t* s_p3) {
+    const ulonglong2 dv = s_il3[j];
+    const uint64_t d = s_p3[j], c1 = c * dv.x;
+    if (c1 * dv.x <= dv.y) return d * (c1 * dv.x);
+    const uint64_t q = exact_sqrt(c1);
+    return q > 1 ? d * q : c;
+}
+
+// rad(c) by one warp, deciding only what the survivor needs (warp-uniform inputs):
+// rad x * base * rad(c) <= 2n requires s(c) = c / rad(c) >= tau = c rad x base / (2n).  c is
+// 1, p, pq, pqr (s = 1), p^2 (s = p), p^3 (s = p^2) or p^2 q (s = p), all primes > P2.
+// Squares and cubes are found exactly; for tau > 1, p^2 q needs p >= t' = max(tau, p1), so
+// either p < q, p in [t', cbrt c], or q < p, q in [p1, c / t'^2] -- the only primes tried
+// (the tau bound is taken 1e-9 low, which only widens the ranges).  A c for which no prime
+// in those ranges divides gets rad = c: squarefree, or p^2 q with p < tau -- rejected either
+// way by the exact R <= 2n test that follows.  tau <= 1: every prime up to cbrt c.
+__device__ uint64_t rad_cofactor_warp(uint64_t c, uint64_t radx, uint64_t base, uint64_t n, const HeavyArgs& a,
+                                      int np2, int np3, const ulonglong2* s_il3, const uint2* s_pd3,
+                                      const uint32_t* s_p3, int lane) {
+    if (c == 1 || c < a.p1sq) return c;  // 1 or a prime
+    if (const uint64_t q = exact_sqrt(c)) return q;
+    const double cd = (double)c;
+    if (c >= a.p1cube) {
+        const uint64_t r = (uint64_t)llrint(cbrt(cd));
+        if (r * r * r == c) return r;
+    } else {
+        return c;  // pq (a square was handled above)
+    }
+    const double tau = cd * (double)radx * (double)base / (2.0 * (double)n);
+    const uint64_t top = (uint64_t)cbrt(cd) + 1;  // p < cbrt c (p < q) or q < cbrt c (q < p)
+    const int i_top = lower_bound_warp(s_p3, np3, top + 1, lane);
+    int j;
+    if (tau <= 1.0 + 1e-6) {
+        j = divisor_in_warp(c, np2, i_top, s_il3, s_pd3, lane);
+    } else {
+        const double tp = fmax(tau * (1.0 - 1e-9), (double)a.p1);
+        if (tp * tp * (double)a.p1 > cd * (1.0 + 1e-9)) return c;  // no p >= t' with q = c / p^2 >= p1
+        const double hb = cd / (tp * tp) * (1.0 + 1e-9) + 1.0;
+        const uint64_t hiB = hb >= (double)top ? top : (uint64_t)hb;
+        const int iB1 = lower_bound_warp(s_p3, np3, hiB + 1, lane);
+        const int iA0 = tp >= (double)top ? i_top : lower_bound_warp(s_p3, np3, (uint64_t)tp, lane);
+        if (iA0 <= iB1) {
+            j = divisor_in_warp(c, np2, i_top, s_il3, s_pd3, lane);
+        } else {
+            j = divisor_in_warp(c, np2, iB1, s_il3, s_pd3, lane);
+            if (j < 0) j = divisor_in_warp(c, iA0, i_top, s_il3, s_pd3, lane);
+        }
+    }
+    return j < 0 ? c : rad_from_divisor(c, j, s_il3, s_p3);
+}
+
+__device__ __forceinline__ void exact_emit(const HeavyArgs& a, bool sideL, uint64_t n, uint64_t radx, uint64_t rady) {
+    if (__umul64hi(radx, rady) != 0 || radx * rady > 2 * n) return;
+    if (sideL) {  // keep from x = n + 1 only if n itself is not heavy
+        const uint64_t y = n, sy = y / rady;
+        if (__umul64hi(2 * sy, sy) != 0 || 2 * sy * sy >= y) return;
+    }
+    emit_candidate(a, sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady});
+}
+
 __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
     // np3 (inv, lim), np3p (inv32, lim32), np3 p, np3p 2^32 mod p (np3p: np3 padded to 32)
     extern __shared__ ulonglong2 s_il3[];
@@ -790,40 +904,30 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t nq = min((uint64_t)a.ctr[CTR_SURV], a.q1_cap);
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-    if (nq * 32 <= nthreads) {
-        // few survivors (domains far from 1): one warp each, the primes spread over the lanes
+    const int np2 = min(a.np2, np3);  // the cofactors hold no prime of index < np2
+    if (a.exact_warp || nq * 32 <= nthreads) {
+        // one warp per survivor, only the primes that can decide it (bounds above ~2^33, or
+        // few survivors)
         const int lane = threadIdx.x & 31;
         for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nq; i += nthreads >> 5) {
-            const ulonglong2 rec = a.q1[i];
-            const bool sideL = rec.x >> 63;
-            const uint64_t n = rec.x & ~(1ull << 63), radx = rec.y;
-            const uint64_t y = sideL ? n : n + 1;
-            const uint64_t rady = rad_warp(y, a.pdiv, a.np3);
-            if (lane) continue;
-            if (__umul64hi(radx, rady) != 0 || radx * rady > 2 * n) continue;
-            if (sideL) {
-                const uint64_t sy = y / rady;
-                if (__umul64hi(2 * sy, sy) != 0 || 2 * sy * sy >= y) continue;
-            }
-            emit_candidate(a, sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady});
+            const BnxSurv rec = a.q1[i];
+            const bool sideL = rec.nside >> 63;
+            const uint64_t n = rec.nside & ~(1ull << 63);
+            const uint64_t radc = rad_cofactor_warp(rec.c, rec.radx, rec.base, n, a, np2, np3, s_il3, s_pd3, s_p3, lane);
+            if (lane == 0) exact_emit(a, sideL, n, rec.radx, rec.base * radc);
         }
         return;
     }
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nq; i += nthreads) {
-        const ulonglong2 rec = a.q1[i];
-        const bool sideL = rec.x >> 63;
-        const uint64_t n = rec.x & ~(1ull << 63), radx = rec.y;
-        const uint64_t y = sideL ? n : n + 1;
-        const int tz = __ffsll((long long)y) - 1;
-        const uint64_t o = y >> tz;
-        const uint64_t rady = (tz ? 2 : 1) * (o < (1ull << 32) ? rad_odd_thread<true>(o, np3, s_il3, s_pd3, s_p3, s_c3)
-                                                               : rad_odd_thread<false>(o, np3, s_il3, s_pd3, s_p3, s_c3));
-        if (__umul64hi(radx, rady) != 0 || radx * rady > 2 * n) continue;
-        if (sideL) {  // keep from x = n + 1 only if n itself is not heavy
-            const uint64_t sy = y / rady;
-            if (__umul64hi(2 * sy, sy) != 0 || 2 * sy * sy >= y) continue;
-        }
-        emit_candidate(a, sideL ? BnxCand{n, rady, radx} : BnxCand{n, radx, rady});
+    const int j_first = np2 & ~31;  // (a block boundary: the primes below np2 no longer divide)
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < nq; i0 += nthreads) {
+        const uint64_t i = i0 + threadIdx.x;
+        const bool live = i < nq;
+        const BnxSurv rec = live ? a.q1[i] : BnxSurv{0, 1, 1, 1};
+        // 32-bit arithmetic when every cofactor of the warp fits (mixed warps would run both)
+        const uint64_t radc = __all_sync(0xFFFFFFFFu, rec.c < (1ull << 32))
+                                  ? rad_cofactor_thread<true>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3)
+                                  : rad_cofactor_thread<false>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3);
+        if (live) exact_emit(a, rec.nside >> 63, rec.nside & ~(1ull << 63), rec.radx, rec.base * radc);
     }
 }
 

@@ -104,7 +104,7 @@ struct HeavyArgs {
     uint64_t p1, p1sq, p1cube;  // P2 + 1 and its powers
     float inv_p1f;
     int cube_filter;        // P2 >= 7: cube residues mod 63 pre-filter the p^3 test
-    ulonglong2* q1;         // screen survivors: (n | side << 63, rad x)
+    BnxSurv* q1;            // stage-1 survivors (n | side << 63, rad x, cofactor, its radical part)
     uint64_t q1_cap;
     BnxCand* cand;          // exact candidates with <= TAIL_HEAVY residue-class members (k_tail)
     uint64_t cand_cap;
@@ -119,6 +119,7 @@ struct HeavyArgs {
     uint32_t run_first;       // k_heavy_screen: share of the items in the first (static) runs, /256
     int* host_flags;          // mapped pinned host flags: [1] k outside its table, [2] a buffer overflowed
     uint32_t sieve_ctas;      // k_heavy_sieve grid (0: the screen's)
+    int exact_warp;           // k_heavy_exact: one warp per survivor, cut prime ranges (else one thread each)
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
 void launch_pdiv32(const BnxPDiv* pdiv, uint64_t n, uint4* out, cudaStream_t st);

@@ -104,6 +104,12 @@ struct BnxPDiv {
 struct BnxCand {
     uint64_t n, r0, r1;
 };
+// A stage-1 survivor of the heavy generator: n with the side bit (63: y = n, else y = n + 1),
+// rad x of the heavy side, and y's odd cofactor after the primes <= P2 with the radical of
+// the part divided off (times 2 if y is even): rad y = base * rad(c).
+struct BnxSurv {
+    uint64_t nside, radx, c, base;
+};
 // One "surplus class" of the heavy-side generator (see bnx_heavy.cu): sigma = m * r with
 // r = rad(sigma), b = sigma * r = m * r^2 (a powerful number); the heavy integers of the class
 // are x = k * b with k squarefree, gcd(k, r) = 1 and k <= 2m.  rmask: which of the first 31

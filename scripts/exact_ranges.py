@@ -42,6 +42,7 @@ def main():
     np3 = sum(1 for p in odd if p <= cb)
     sp = oracle.primes_up_to(math.isqrt(hi + 2) + 1)
     stats = {"reject_B": 0, "full": 0, "sqcube": 0, "cut": 0}
+    blocks = []  # (t, blocks needed) of the cut survivors
     work, surv = [], 0
     step = 1 << 24
     for base in range(lo, hi + 1, step):
@@ -102,6 +103,11 @@ def main():
                 top = icbrt(c)
                 lo_b, hi_b = p1, min(top, c // (tp * tp))
                 lo_a, hi_a = tp, top - 1
+                # 32-prime blocks (from index np2) a lane needs
+                ib = bisect.bisect_right(odd, hi_b)
+                ia0, ia1 = bisect.bisect_left(odd, lo_a), bisect.bisect_right(odd, top)
+                need = set(range(np2 // 32, (ib + 31) // 32)) | set(range(ia0 // 32, (ia1 + 31) // 32))
+                blocks.append((tau_of := t, need))
                 segs = sorted(s for s in ((lo_a, hi_a), (lo_b, hi_b)) if s[0] <= s[1])
                 cnt, cur = 0, 0
                 for a, b in segs:
@@ -114,9 +120,28 @@ def main():
     rng = np.random.default_rng(0)
     perm = rng.permutation(len(wk))
     warps = wk[perm][: len(wk) // 32 * 32].reshape(-1, 32).max(axis=1) if len(wk) >= 32 else wk
+    # the same warps after sorting each group of 256 survivors (one CTA) by its range
+    g = wk[perm][: len(wk) // 256 * 256].reshape(-1, 256) if len(wk) >= 256 else wk[perm].reshape(1, -1)
+    gs = np.sort(g, axis=1)
+    sorted_max = gs[:, : gs.shape[1] // 32 * 32].reshape(-1, 32).max(axis=1) if gs.shape[1] >= 32 else gs.max(axis=1)
+    # warps iterating the global blocks, skipping a block no lane needs: after sorting each
+    # group of 256 by t, the blocks a warp runs (union of its lanes) against all of np2..np3
+    nb_all = (np3 + 31) // 32 - np2 // 32
+    order = rng.permutation(len(blocks))
+    bl = [blocks[i] for i in order]
+    unions = []
+    for g0 in range(0, len(bl) - 255, 256):
+        grp = sorted(bl[g0:g0 + 256], key=lambda r: r[0])
+        for w0 in range(0, 256, 32):
+            u = set()
+            for _, nd in grp[w0:w0 + 32]:
+                u |= nd
+            unions.append(len(u))
+    print({"blocks_all": nb_all, "warp_union_sorted": round(float(np.mean(unions)), 2) if unions else None})
     print({"S": f"2^{e}", "window": f"2^{w}", "survivors": surv, **stats, "np2": np2, "np3": np3,
            "mean_primes": round(float(wk.mean()), 1) if len(wk) else 0,
-           "mean_warp_max": round(float(warps.mean()), 1) if len(wk) else 0})
+           "mean_warp_max": round(float(warps.mean()), 1) if len(wk) else 0,
+           "mean_warp_max_sorted256": round(float(sorted_max.mean()), 1) if len(wk) else 0})
 
 
 if __name__ == "__main__":

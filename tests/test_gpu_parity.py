@@ -446,3 +446,28 @@ def test_sieve_mask_mode_at_small_bounds(orc, monkeypatch, kmin):
         assert st["survivors"] == base.stats()["survivors"] and st["candidates"] == 2253
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_exact_stage_modes(orc, monkeypatch, mode):
+    """k_heavy_exact one thread per survivor (0: every prime from P2 to cbrt y) or one warp per
+    survivor (1: only the primes that can complete a p^2 q factor large enough), each forced
+    on both sides of the default switch: exact candidate counts against the oracle's sieve
+    and the same rows as the default context, near 2^32, 2^40, 1.4e12 and 2^46, and the
+    whole 2^32 search."""
+    from paper_2506_01099_b200 import _native
+
+    base = _native.context(0)
+    monkeypatch.setenv("BNX_EXACT_WARP", mode)
+    ctx = _native.Context(0)
+    try:
+        for lo, hi in [(1, 2**22), (2**32 - 2**21, 2**32 + 2**21), (2**40 - 2**21, 2**40 - 1),
+                       (1_400_000_000_000 - 2**21, 1_400_000_000_000), (2**46 - 2**20, 2**46 - 2)]:
+            got = ctx.search_domain(lo, hi, 3, None, 0)
+            assert ctx.stats()["candidates"] == exact_candidates(orc, lo, hi), (mode, lo, hi)
+            assert got.tobytes() == base.search_domain(lo, hi, 3, None, 0).tobytes(), (mode, lo, hi)
+        got = ctx.search(2**32, 3, None, 0)
+        assert got.tobytes() == base.search(2**32, 3, None, 0).tobytes()
+        assert ctx.stats()["candidates"] == 2253
+    finally:
+        ctx.close()
