@@ -1008,10 +1008,11 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
             cudaStreamWaitEvent(aux, ev_fork, 0);
             const size_t smemS = heavy_sieve_smem(a.np2, a.kc, a.ntasks);
             const int sgrid = a.sieve_ctas ? (int)a.sieve_ctas : grid;
+            const int sthreads = a.sieve_threads ? (int)a.sieve_threads : 256;
             if (heavy_sieve_mask(a.np2))
-                k_heavy_sieve<true><<<sgrid, 256, smemS, aux>>>(a);
+                k_heavy_sieve<true><<<sgrid, sthreads, smemS, aux>>>(a);
             else
-                k_heavy_sieve<false><<<sgrid, 256, smemS, aux>>>(a);
+                k_heavy_sieve<false><<<sgrid, sthreads, smemS, aux>>>(a);
             cudaEventRecord(ev_join, aux);
         }
         const size_t np2p = (size_t)(a.np2 + 31) & ~(size_t)31;  // (see k_heavy_screen)

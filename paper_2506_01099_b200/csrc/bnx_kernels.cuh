@@ -119,6 +119,7 @@ struct HeavyArgs {
     uint32_t run_first;       // k_heavy_screen: share of the items in the first (static) runs, /256
     int* host_flags;          // mapped pinned host flags: [1] k outside its table, [2] a buffer overflowed
     uint32_t sieve_ctas;      // k_heavy_sieve grid (0: the screen's)
+    uint32_t sieve_threads;   // k_heavy_sieve CTA size (0: 256)
     int exact_warp;           // k_heavy_exact: one warp per survivor, cut prime ranges (else one thread each)
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
