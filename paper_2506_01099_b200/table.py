@@ -4,8 +4,11 @@ Device counterpart of the reference's ``SignatureTable`` (chunked.py:129-304,
 _kernels.py:130-232) and of its per-chunk search (chunked.py:307-359): open addressing with
 the reference's slot word ((t+1) << 32 | home, 0 = empty), its commutative hash and linear
 probing, but built by all GPU threads at once with 64-bit CAS.  The pair set equals the
-serial build's; slot placement can differ, and the pairs come back sorted ((n, m) for
-builds, (m, n) for probes) instead of in serial discovery order.
+serial build's and slot placement can differ; the pairs come back in the serial build's
+discovery order all the same, restored by sorting: the serial build meets the stored entries
+of one signature in insertion order along their probe chain, so its matches are ordered by
+(n, m), and a serial probe's by (m, n) (the reference's golden lists, checked in order by
+tests/test_gpu_table.py).
 
 This path exists for an apples-to-apples comparison with the paper's method (it is
 quadratic in the limit, like the reference); the production search is ``search.py``.
