@@ -98,6 +98,8 @@ struct Tables {
     int nitems = 0;
     uint32_t nsmall = 0;
     uint64_t nlarge = 0, npdiv = 0;
+    uint64_t nmedium = 0;  // large[0, nmedium): q < SIEVE_HUGE_Q, once `split` (exact sieve)
+    bool split = false;
     void release() {
         small.release();
         large.release();
@@ -198,6 +200,10 @@ struct bnx_ctx {
     int sieve_v = 0;
     int sieve_nv = 0;              // 32-bit-slot geometry for windows below 2^32 (BNX_SIEVE_NARROW; -1: off)
     int sieve_narrow_blocks_per_sm = 1;
+    bool sieve_gbuckets = true;    // large progressions bucketed per window (BNX_SIEVE_GBUCKETS=0: per-segment scan)
+    DBuf<uint64_t> sieve_gbuck;
+    DBuf<uint32_t> sieve_gcnt;
+    DBuf<unsigned long long> t_split;
 
     // prime table (device u32 + host mirror)
     DBuf<uint32_t> primes;
@@ -524,6 +530,8 @@ int build_tables(bnx_ctx* c, Tables& t, uint64_t max_x, int include_two, uint32_
     t.include_two = include_two;
     t.tile = tile;
     t.nwarps = nwarps;
+    t.split = false;
+    t.nmedium = 0;
     t.gen = c->gen;
     return BNX_OK;
 }
@@ -1231,6 +1239,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
         CK(cudaFuncSetAttribute(sv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sv.smem));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_narrow_blocks_per_sm, sv.fn, sv.threads, sv.smem));
     }
+    if (const char* env = std::getenv("BNX_SIEVE_GBUCKETS")) c->sieve_gbuckets = std::atoi(env) != 0;
     c->sieve_blocks_per_sm = std::max(1, c->sieve_blocks_per_sm);
     c->sieve_narrow_blocks_per_sm = std::max(1, c->sieve_narrow_blocks_per_sm);
     *out = c;
@@ -1258,7 +1267,10 @@ int bnx_ctx_destroy(bnx_ctx_t* c) {
     c->t_nlarge.release();
     c->t_npdiv.release();
     c->t_over.release();
+    c->t_split.release();
     c->sieve_out.release();
+    c->sieve_gbuck.release();
+    c->sieve_gcnt.release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->kev)
@@ -1395,20 +1407,59 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
     const bool narrow = c->sieve_nv >= 0 && end < (1ull << 32);
     const SieveVariant& sv = narrow ? sieve_narrow(c->sieve_nv) : sieve_variant(c->sieve_v);
     const int bps = narrow ? c->sieve_narrow_blocks_per_sm : c->sieve_blocks_per_sm;
+    // global buckets for the huge progressions above 2^32 (below, at most ~6,500 large
+    // progressions: the per-segment scan is cheaper than the extra pass)
+    for (bool gbuckets = c->sieve_gbuckets && !narrow;; gbuckets = false) {
     TRY(build_tables(c, c->sieve_tab, end, fast ? 0 : 1, (uint32_t)sv.tile, sv.threads / 32));
     if (c->sieve_tab.nsmall > (uint32_t)SIEVE_MAXS) return fail(BNX_ERR_CUDA, "too many small progressions");
     TRY(c->flags.ensure(4));
     if (!c->h_flags) CK(cudaMallocHost(&c->h_flags, sizeof(int) * 4));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
-    const uint64_t piece = out_dev ? length : std::min<uint64_t>(length, 1ull << 27);
+    const uint64_t piece = out_dev ? std::min<uint64_t>(length, 1ull << 32) : std::min<uint64_t>(length, 1ull << 27);
     if (!out_dev) TRY(c->sieve_out.ensure(piece));
     const uint64_t SEG = (uint64_t)sv.tile * sv.nt;
+    // global buckets for the large progressions: SEG / 128 entries per segment, ~2.8x the
+    // expected hits (the sum over q >= the tile of SEG / q is below SEG / 350); a full one
+    // re-runs the call with the per-segment scan
+    const uint32_t gcap = (uint32_t)(SEG / 128);
+    const uint64_t nseg_max = (piece + SEG - 1) / SEG;
+    if (gbuckets) {
+        TRY(c->sieve_gcnt.ensure(nseg_max));
+        TRY(c->sieve_gbuck.ensure(nseg_max * gcap));
+        Tables& t = c->sieve_tab;
+        if (!t.split && t.nlarge) {  // medium progressions to the front, huge ones to the back (once per table)
+            DBuf<BnxProg> tmp;
+            TRY(tmp.ensure(t.nlarge));
+            TRY(c->t_split.ensure(2));
+            CK(cudaMemsetAsync(c->t_split.p, 0, 2 * sizeof(unsigned long long), c->stream));
+            launch_split_large(t.large.p, t.nlarge, tmp.p, c->t_split.p, c->stream);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(t.large.p, tmp.p, sizeof(BnxProg) * t.nlarge, cudaMemcpyDeviceToDevice, c->stream));
+            unsigned long long nm = 0;
+            CK(cudaMemcpyAsync(&nm, c->t_split.p, sizeof(nm), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            tmp.release();
+            t.nmedium = nm;
+            t.split = true;
+        } else if (!t.nlarge) {
+            t.split = true;
+        }
+    }
     for (uint64_t off = 0; off < length; off += piece) {
         const uint64_t len = std::min<uint64_t>(piece, length - off);
-        uint64_t* dst = out_dev ? out_dev : c->sieve_out.p;
+        uint64_t* dst = out_dev ? out_dev + off : c->sieve_out.p;
         SieveArgs sa{start + off, len, c->sieve_tab.small.p, (int)c->sieve_tab.nsmall, c->sieve_tab.large.p,
-                     c->sieve_tab.nlarge, c->sieve_tab.items.p, c->sieve_tab.nitems, fast, dst, c->flags.p};
+                     c->sieve_tab.nlarge, c->sieve_tab.items.p, c->sieve_tab.nitems, fast, dst, c->flags.p,
+                     nullptr, nullptr, 0, 0};
         const uint64_t nseg = (len + SEG - 1) / SEG;
+        if (gbuckets && sa.nlarge) {
+            CK(cudaMemsetAsync(c->sieve_gcnt.p, 0, sizeof(uint32_t) * nseg, c->stream));
+            sa.gbuck = c->sieve_gbuck.p;
+            sa.gcnt = c->sieve_gcnt.p;
+            sa.gcap = gcap;
+            sa.nmedium = c->sieve_tab.nmedium;
+            launch_sieve_buckets(sa, SEG, c->sieve_gbuck.p, c->sieve_gcnt.p, c->stream);
+        }
         const int grid = (int)std::min<uint64_t>(nseg, (uint64_t)c->num_sms * bps);
         sv.launch(sa, grid, c->stream);
         CK(cudaGetLastError());
@@ -1417,7 +1468,12 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
     CK(cudaMemcpyAsync(c->h_flags, c->flags.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (c->h_flags[0]) return fail(BNX_ERR_CUDA, "sieve bucket overflow");
+    if (gbuckets && c->h_flags[3]) {  // a full global bucket: again with the per-segment scan
+        CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 4, c->stream));
+        continue;
+    }
     return BNX_OK;
+    }
 }
 
 int bnx_sieve_radicals(bnx_ctx_t* c, uint64_t start, uint64_t length, const uint64_t* primes, size_t nprimes,

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "bnx_kernels.cuh"
@@ -588,15 +589,35 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
         for (int j = tid; j < NT; j += THREADS) bcnt[j] = 0;
         for (int j = tid; j < nsmall; j += THREADS) s_off[j] = (uint32_t)bnx_first_offset(seg0, s_q[j], a.small[j].recip);
         __syncthreads();
-        for (uint64_t j = tid; j < a.nlarge; j += THREADS) {
-            const BnxProg pr = a.large[j];
-            uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip);
-            while (o < SEG) {
-                const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
+        // (windows below 2^32 -- NARROW -- always scan: the host buckets only above)
+        if (!NARROW && a.gbuck) {  // the medium progressions here, the huge ones' hits from the window's buckets
+            for (uint64_t j = tid; j < a.nmedium; j += THREADS) {
+                const BnxProg pr = a.large[j];
+                for (uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip); o < SEG; o += pr.q) {
+                    const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
+                    uint32_t k = atomicAdd(&bcnt[t], 1u);
+                    if (k < BCAP) bent[t * BCAP + k] = ((uint64_t)pr.p << 16) | loc; else a.flags[0] = 1;
+                }
+            }
+            const uint32_t nh = min(a.gcnt[seg], a.gcap);
+            const uint64_t* gb = a.gbuck + seg * (uint64_t)a.gcap;
+            for (uint32_t i = tid; i < nh; i += THREADS) {
+                const uint64_t e = gb[i];
+                const uint32_t o = (uint32_t)e, t = o / TILE, loc = o % TILE;
                 uint32_t k = atomicAdd(&bcnt[t], 1u);
-                if (k < BCAP) bent[t * BCAP + k] = ((uint64_t)pr.p << 16) | loc; else a.flags[0] = 1;
-                if (pr.q >= SEG) break;
-                o += pr.q;
+                if (k < BCAP) bent[t * BCAP + k] = ((e >> 32) << 16) | loc; else a.flags[0] = 1;
+            }
+        } else {
+            for (uint64_t j = tid; j < a.nlarge; j += THREADS) {
+                const BnxProg pr = a.large[j];
+                uint64_t o = bnx_first_offset(seg0, pr.q, pr.recip);
+                while (o < SEG) {
+                    const uint32_t t = (uint32_t)(o / TILE), loc = (uint32_t)(o % TILE);
+                    uint32_t k = atomicAdd(&bcnt[t], 1u);
+                    if (k < BCAP) bent[t * BCAP + k] = ((uint64_t)pr.p << 16) | loc; else a.flags[0] = 1;
+                    if (pr.q >= SEG) break;
+                    o += pr.q;
+                }
             }
         }
         __syncthreads();
@@ -1138,6 +1159,41 @@ __global__ void __launch_bounds__(256) k_table_quad(TableArgs a) {
             }
         }
     }
+}
+
+// Global buckets of the huge progressions (q >= SIEVE_HUGE_Q, above every segment length): a
+// thread per progression walks its few hits in the window once and appends each to the
+// bucket of its segment, so a segment reads its hits instead of testing every progression
+// (the per-segment scan costs O(segments x pi(sqrt end)): 0.8 s for 2^30 integers at 2^62).
+__global__ void k_sieve_buckets(SieveArgs a, uint64_t seg_len, uint64_t* gbuck, uint32_t* gcnt, uint32_t gcap) {
+    for (uint64_t j = a.nmedium + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < a.nlarge;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const BnxProg pr = a.large[j];
+        for (uint64_t o = bnx_first_offset(a.start, pr.q, pr.recip); o < a.length; o += pr.q) {
+            const uint64_t seg = o / seg_len;
+            const uint32_t k = atomicAdd(&gcnt[seg], 1u);
+            if (k < gcap) gbuck[seg * gcap + k] = ((uint64_t)pr.p << 32) | (o - seg * seg_len);
+            else a.flags[3] = 1;
+            if (pr.q > a.length) break;
+        }
+    }
+}
+void launch_sieve_buckets(const SieveArgs& a, uint64_t seg_len, uint64_t* gbuck, uint32_t* gcnt, cudaStream_t st) {
+    if (a.nlarge <= a.nmedium) return;
+    const unsigned grid = (unsigned)std::min<uint64_t>((a.nlarge - a.nmedium + 255) / 256, 148 * 16);
+    k_sieve_buckets<<<grid, 256, 0, st>>>(a, seg_len, gbuck, gcnt, a.gcap);
+}
+// Order-free split of the large progressions: q < SIEVE_HUGE_Q to the front of `out`, the
+// rest to the back (counts[0], counts[1]).
+__global__ void k_split_large(const BnxProg* in, uint64_t n, BnxProg* out, unsigned long long* counts) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const BnxProg pr = in[j];
+        if (pr.q < SIEVE_HUGE_Q) out[atomicAdd(&counts[0], 1ull)] = pr;
+        else out[n - 1 - atomicAdd(&counts[1], 1ull)] = pr;
+    }
+}
+void launch_split_large(const BnxProg* in, uint64_t n, BnxProg* out, unsigned long long* counts, cudaStream_t st) {
+    if (n) k_split_large<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(in, n, out, counts);
 }
 
 // ------------------------------------------------------------------------------------

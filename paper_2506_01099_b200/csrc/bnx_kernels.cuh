@@ -162,7 +162,22 @@ struct SieveArgs {
     int fast;
     uint64_t* out;
     int* flags;
+    // the large progressions' hits, pre-sorted by segment (launch_sieve_buckets): entry
+    // p << 32 | offset in the segment, gcnt[seg] of them at gbuck + seg * gcap; null: each
+    // segment scans all large progressions itself
+    const uint64_t* gbuck;
+    const uint32_t* gcnt;
+    uint32_t gcap;
+    uint64_t nmedium;  // with gbuck: large[0, nmedium) (q < SIEVE_HUGE_Q) are scanned per segment,
+                       // the rest come from the buckets
 };
+constexpr uint64_t SIEVE_HUGE_Q = 1ull << 24;  // above every segment length (at most one hit per segment, 64 per 2^30)
+// The large progressions split in place order-free: q < SIEVE_HUGE_Q to the front, the rest
+// to the back of `out` (n entries); *nmed = the front count.
+void launch_split_large(const BnxProg* in, uint64_t n, BnxProg* out, unsigned long long* counts, cudaStream_t st);
+// One pass over the large progressions of a window: every hit appended to its segment's
+// global bucket (flags[3] on a full bucket).
+void launch_sieve_buckets(const SieveArgs& a, uint64_t seg_len, uint64_t* gbuck, uint32_t* gcnt, cudaStream_t st);
 
 // Compiled screen geometries (tile, tiles per segment, threads, bucket capacity); the
 // context picks one at creation (BNX_SCREEN_VARIANT, default 0).
@@ -208,6 +223,7 @@ int sieve_variant_count();
 const SieveVariant& sieve_variant(int i);
 int sieve_narrow_count();  // the same kernel with 32-bit slots (windows ending below 2^32)
 const SieveVariant& sieve_narrow(int i);
+
 void launch_tail(const TailArgs& a, int grid, cudaStream_t st);
 void launch_tail_light(const TailArgs& a, int grid, cudaStream_t st, bool pdl = false);  // heavy engine: k_tail only
 void launch_tail_heavy(const TailArgs& a, cudaStream_t st);            // heavy engine: k_tail_heavy only

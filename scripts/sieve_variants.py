@@ -2,7 +2,9 @@
 in its own process, time k_sieve_exact over [1, 2^30] (min of 5, CUDA events, L2 flushed)
 and hash the output plus two windows high in the range, so the variants can be compared
 for speed and for identical radicals.  Prints one JSON line per variant.  [1, 2^30] runs the
-32-bit-slot geometry BNX_SIEVE_NARROW (default 0; -1: the u64 variant itself)."""
+32-bit-slot geometry BNX_SIEVE_NARROW (default 0; -1: the u64 variant itself); SIEVE_START
+moves the timed window (e.g. 2^40, 2^62: u64 slots, huge progressions bucketed per window,
+BNX_SIEVE_GBUCKETS)."""
 import hashlib
 import json
 import os
@@ -24,14 +26,15 @@ def child() -> None:
     ctx.set_stream(s.cuda_stream)
     flush = torch.empty(1 << 26, dtype=torch.int32, device="cuda")
     n = 1 << 30
+    start0 = int(eval(os.environ.get("SIEVE_START", "1").replace("^", "**")))  # timed window [start0, start0 + 2^30)
     out = torch.empty(n, dtype=torch.int64, device="cuda")
-    ctx.sieve_radicals_dev(1, n, out.data_ptr())
+    ctx.sieve_radicals_dev(start0, n, out.data_ptr())
     times = []
     for k in range(5):
         flush.fill_(k)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
-        ctx.sieve_radicals_dev(1, n, out.data_ptr())
+        ctx.sieve_radicals_dev(start0, n, out.data_ptr())
         b.record(s)
         b.synchronize()
         times.append(a.elapsed_time(b))
@@ -48,7 +51,8 @@ def child() -> None:
         hi.append(hashlib.sha256(out[1:m + 1].cpu().numpy().tobytes()).hexdigest()[:16])
     ms = min(times)
     print(json.dumps({"variant": os.environ.get("BNX_SIEVE_VARIANT", "0"),
-                      "narrow": os.environ.get("BNX_SIEVE_NARROW", "0"), "ms": ms,
+                      "narrow": os.environ.get("BNX_SIEVE_NARROW", "0"),
+                      "start": start0, "ms": ms,
                       "GBps": 8 * n / (ms / 1e3) / 1e9, "times": times, "sha_2p30": h, "sha_high": hi}))
 
 

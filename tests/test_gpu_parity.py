@@ -98,6 +98,31 @@ def test_sieve_narrow_slots_vs_oracle(orc, monkeypatch, variant):
         ctx.close()
 
 
+@pytest.mark.parametrize("gbuckets", ["0", "1"])
+def test_sieve_global_buckets_vs_oracle(orc, monkeypatch, gbuckets):
+    """Windows reaching 2^32 take the huge progressions' hits from one bucketing pass over the
+    window (BNX_SIEVE_GBUCKETS=1, default) or scan them per segment (0): windows straddling
+    2^32, at prime powers with large surpluses (3^22, 5^15, 2 * 7^13), random windows up to
+    2^40, several segments and a ragged end, both ctz modes, against the oracle."""
+    from paper_2506_01099_b200 import _native
+
+    monkeypatch.setenv("BNX_SIEVE_GBUCKETS", gbuckets)
+    ctx = _native.Context(0)
+    try:
+        rng = np.random.default_rng(int(gbuckets) + 11)
+        cases = [(2**32 - 2**20 + 3, 2**21 + 9), (2**32, 5), (3**22 - 5000, 10001), (5**15 - 77, 300),
+                 (2 * 7**13 - 3, 100), (2**36 - 2**19, 3 * 2**20 + 17)]
+        cases += [(int(rng.integers(2**32, 2**40)), int(rng.integers(1, 2**21))) for _ in range(6)]
+        for start, length in cases:
+            for fast in (True, False):
+                need = math.isqrt(start + length - 1)
+                got = ctx.sieve_radicals(start, length, None, 0, fast)
+                want = orc.sieve_segment(start, length, orc.primes_up_to(need + 1), fast)
+                assert np.array_equal(got, want), (gbuckets, start, length, fast)
+    finally:
+        ctx.close()
+
+
 # ---------------------------------------------------------------- trial division ---------
 def test_trial_division_vectors(golden):
     for rec in golden["trial_division"]:
