@@ -62,6 +62,8 @@ __device__ __forceinline__ uint64_t exact_sqrt(uint64_t c) {
 // decides), so the p^2 q case uses a rounded-up float root; squares and cubes are detected
 // exactly (rounded roots checked in integers, see exact_sqrt; the cube root of c < 2^50 is
 // below 2^17, where cbrtf's error is < 0.02).
+__device__ __forceinline__ float approx_rsqrt(float x);
+__device__ __forceinline__ float approx_cbrt(float x);
 __device__ __forceinline__ uint64_t surplus_bound(uint64_t c, const HeavyArgs& a) {
     if (c < a.p1sq) return 1;  // 1 or a prime
     uint64_t u = 1;
@@ -71,12 +73,17 @@ __device__ __forceinline__ uint64_t surplus_bound(uint64_t c, const HeavyArgs& a
         if (q) u = q;
     }
     if (c >= a.p1cube) {
-        const uint64_t v = (uint64_t)(sqrtf(cf * a.inv_p1f) * 1.0001f) + 1;  // >= sqrt(c / p1)
+        // >= sqrt(c / p1): the MUFU root's relative error (~1e-6) is inside the 1.0001 margin
+        const float t = cf * a.inv_p1f;
+        const uint64_t v = (uint64_t)(t * approx_rsqrt(t) * 1.0001f) + 1;
         if (v > u) u = v;
-        // p^3 with p > P2 >= 7: p^3 = +-1 mod 7 and mod 9, i.e. c mod 63 in {1, 8, 55, 62}
-        const uint32_t m63 = (uint32_t)(c % 63u);
+        // p^3 with p > P2 >= 7: p^3 = +-1 mod 7 and mod 9, i.e. c mod 63 in {1, 8, 55, 62};
+        // c mod 63 from the 32-bit halves (2^32 = 4 mod 63; c < 2^53: hi < 2^21)
+        const uint32_t lo = (uint32_t)c, hi = (uint32_t)(c >> 32);
+        const uint32_t m63 = (4u * hi + lo % 63u) % 63u;
         if (!a.cube_filter || m63 == 1 || m63 == 8 || m63 == 55 || m63 == 62) {
-            const uint64_t r = (uint64_t)rintf(cbrtf(cf));
+            // a cube below 2^53 has its root below 2^18: the MUFU cube root lands within 0.3
+            const uint64_t r = (uint64_t)rintf(c < (1ull << 45) ? approx_cbrt(cf) : cbrtf(cf));
             if (r * r * r == c && r * r > u) u = r * r;
         }
     }
