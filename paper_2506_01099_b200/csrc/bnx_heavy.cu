@@ -247,7 +247,8 @@ struct HeavyItem {
 template <bool NARROW, bool SIEVED = false>
 __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
                                              const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32,
-                                             const uint32_t* sm = nullptr, int stride = 0) {
+                                             const uint32_t* sm = nullptr, int stride = 0,
+                                             const uint32_t* s_e32 = nullptr) {
     using W = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     const uint64_t x = it.x;
     const bool vL = x >= 2 && x - 1 >= a.n_first && x - 1 <= a.n_last;
@@ -258,6 +259,9 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
     W sL = tL ? (W)1 << (tL - 1) : (W)1, sU = tU ? (W)1 << (tU - 1) : (W)1;
     W rL = tL ? (W)2 : (W)1, rU = tU ? (W)2 : (W)1;  // radicals of the divided-off parts
     const uint32_t x32 = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    // x >= 2^32: W = x_lo + x_hi (2^32 mod p) = x (mod p) stays below 2^32 - 1 for every
+    // stage-1 prime (all below p1) unless x_lo is within x_hi p1 of 2^32 (rare)
+    const bool nowrap = s_e32 && xh < 65536u && x32 < 0xFFFFFFFFu - xh * (uint32_t)a.p1;
     // Divisibility by 32 primes at a time into a bit mask, branch-free (the lanes of a warp
     // stay converged): one bit per prime for both sides (an odd p divides at most one of
     // x - 1, x + 1), the side is found in the post-pass.  The table is padded to a multiple
@@ -275,6 +279,16 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
                 const uint2 d = s_pd32[j0 + u];
                 const uint32_t t = x32 * d.x;
                 m |= (uint32_t)(min(t - d.x, t + d.x) <= d.y) << u;
+            }
+        } else if (nowrap) {
+            // (W -+ 1) p^-1 = (x_lo -+ 1) p^-1 + x_hi e (mod 2^32), e = (2^32 mod p) p^-1: three
+            // multiply-adds per prime for both sides, exact since 0 <= W - 1, W + 1 < 2^32
+            const uint32_t xm = x32 - 1u, xp = x32 + 1u;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const uint2 d = s_pd32[j0 + u];
+                const uint32_t h = xh * s_e32[j0 + u];
+                m |= (uint32_t)(min(xm * d.x + h, xp * d.x + h) <= d.y) << u;
             }
         } else {
             // x >= 2^32 (x < 2^53): w = x_lo + x_hi (2^32 mod p) is x mod p shifted into 32
@@ -338,11 +352,12 @@ __device__ __forceinline__ void y_tests_impl(const HeavyArgs& a, const HeavyItem
 }
 
 __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it, const ulonglong2* s_il,
-                                        const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32) {
+                                        const uint32_t* s_p, const uint2* s_pd32, const uint32_t* s_c32,
+                                        const uint32_t* s_e32) {
     if (it.x + 1 < (1ull << 32))
         y_tests_impl<true>(a, it, s_il, s_p, s_pd32, s_c32);
     else
-        y_tests_impl<false>(a, it, s_il, s_p, s_pd32, s_c32);
+        y_tests_impl<false>(a, it, s_il, s_p, s_pd32, s_c32, nullptr, 0, s_e32);
 }
 
 // Each CTA owns a contiguous run of items and walks it in windows of HEAVY_THREADS (thread t
@@ -357,6 +372,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     uint2* s_pd32 = reinterpret_cast<uint2*>(s_il + a.np2);
     uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + np2p);
     uint32_t* s_c32 = s_p + a.np2;
+    uint32_t* s_e32 = s_c32 + np2p;  // (2^32 mod p) p^-1 mod 2^32
     __shared__ HeavyItem s_q[2 * T];
     __shared__ uint64_t s_end[T];  // class ends of a multi-class window
     __shared__ int s_cnt;
@@ -368,10 +384,12 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         s_pd32[j] = make_uint2(q.x, q.y);
         s_p[j] = q.z;
         s_c32[j] = q.w;
+        s_e32[j] = q.w * q.x;
     }
     for (int j = a.np2 + tid; j < np2p; j += T) {  // padding (its bits are masked off)
         s_pd32[j] = make_uint2(1u, 0u);
         s_c32[j] = 0u;
+        s_e32[j] = 0u;
     }
     if (tid == 0) s_cnt = 0;
     // k_heavy_exact may be scheduled now (programmatic dependent launch): its CTAs take the
@@ -468,7 +486,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         }
         if (cnt == 0) break;
         const int take = min(cnt, T);
-        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p, s_pd32, s_c32);
+        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p, s_pd32, s_c32, s_e32);
         cnt -= take;
         __syncthreads();
         if (tid == 0) s_cnt = cnt;
@@ -1024,7 +1042,7 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
         }
         const size_t np2p = (size_t)(a.np2 + 31) & ~(size_t)31;  // (see k_heavy_screen)
         const size_t smem2 = (size_t)a.np2 * (sizeof(ulonglong2) + sizeof(uint32_t)) +
-                             np2p * (sizeof(uint2) + sizeof(uint32_t));
+                             np2p * (sizeof(uint2) + 2 * sizeof(uint32_t));
         if (kev) cudaEventRecord(kev[1], st);
         if (stop_after == 1) {
             if (kev) for (int i = 2; i < 4; ++i) cudaEventRecord(kev[i], st);
