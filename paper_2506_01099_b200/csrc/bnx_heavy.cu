@@ -751,7 +751,8 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
 // NARROW: c < 2^32, everything in 32-bit arithmetic.
 template <bool NARROW>
 __device__ __forceinline__ uint64_t rad_cofactor_thread(uint64_t o, int j_first, int np3, const ulonglong2* s_il3,
-                                                        const uint2* s_pd3, const uint32_t* s_p3, const uint32_t* s_c3) {
+                                                        const uint2* s_pd3, const uint32_t* s_p3, const uint32_t* s_e3,
+                                                        bool nowrap = false) {
     using W = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     W c = (W)o, rad = 1;
     const uint32_t ol = (uint32_t)o, oh = (uint32_t)(o >> 32);
@@ -764,11 +765,17 @@ __device__ __forceinline__ uint64_t rad_cofactor_thread(uint64_t o, int j_first,
                 const uint2 d = s_pd3[j0 + u];
                 m |= (uint32_t)(ol * d.x <= d.y) << u;
             }
+        } else if (nowrap) {  // W = ol + oh (2^32 mod p) < 2^32: W p^-1 = ol p^-1 + oh e (mod 2^32)
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const uint2 d = s_pd3[j0 + u];
+                m |= (uint32_t)(ol * d.x + oh * s_e3[j0 + u] <= d.y) << u;
+            }
         } else {  // o = oh 2^32 + ol: w = ol + oh (2^32 mod p) = o (mod p) in 32 bits (p, oh < 2^16)
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
                 const uint2 d = s_pd3[j0 + u];
-                const uint32_t cp = s_c3[j0 + u];
+                const uint32_t cp = s_e3[j0 + u] * s_p3[j0 + u];  // (e p = 2^32 mod p)
                 uint32_t w = ol + oh * cp;
                 if (w < ol) w += cp;
                 m |= (uint32_t)(w * d.x <= d.y) << u;
@@ -904,7 +911,8 @@ __device__ __forceinline__ void exact_emit(const HeavyArgs& a, bool sideL, uint6
 }
 
 __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
-    // np3 (inv, lim), np3p (inv32, lim32), np3 p, np3p 2^32 mod p (np3p: np3 padded to 32)
+    // np3 (inv, lim), np3p (inv32, lim32), np3 p, np3p e = (2^32 mod p) p^-1 mod 2^32 (np3p:
+    // np3 padded to 32)
     extern __shared__ ulonglong2 s_il3[];
     const int np3 = (int)a.np3, np3p = (np3 + 31) & ~31;
     uint2* s_pd3 = reinterpret_cast<uint2*>(s_il3 + np3);
@@ -915,13 +923,14 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         const uint4 q = a.pd32[j];
         s_pd3[j] = make_uint2(q.x, q.y);
         s_p3[j] = q.z;
-        s_c3[j] = q.w;
+        s_c3[j] = q.w * q.x;
     }
     for (int j = np3 + threadIdx.x; j < np3p; j += blockDim.x) {  // padding (its bits are masked off)
         s_pd3[j] = make_uint2(1u, 0u);
         s_c3[j] = 0u;
     }
     __syncthreads();
+    const uint64_t pmax = np3 ? s_p3[np3 - 1] : 1;
     // launched as a programmatic dependent of k_heavy_screen: the tables above overlap its
     // last CTAs; the survivors are read only after it has completed (and flushed).  k_tail
     // (one-graph searches) may in turn be scheduled from here.
@@ -948,10 +957,13 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         const uint64_t i = i0 + threadIdx.x;
         const bool live = i < nq;
         const BnxSurv rec = live ? a.q1[i] : BnxSurv{0, 1, 1, 1};
-        // 32-bit arithmetic when every cofactor of the warp fits (mixed warps would run both)
-        const uint64_t radc = __all_sync(0xFFFFFFFFu, rec.c < (1ull << 32))
-                                  ? rad_cofactor_thread<true>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3)
-                                  : rad_cofactor_thread<false>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3);
+        // 32-bit arithmetic when every cofactor of the warp fits (mixed warps would run both);
+        // above, the one-step reduction when no cofactor of the warp can wrap
+        const uint64_t radc =
+            __all_sync(0xFFFFFFFFu, rec.c < (1ull << 32))
+                ? rad_cofactor_thread<true>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3)
+                : rad_cofactor_thread<false>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3,
+                                             __all_sync(0xFFFFFFFFu, (rec.c & 0xFFFFFFFFull) + (rec.c >> 32) * pmax < (1ull << 32)));
         if (live) exact_emit(a, rec.nside >> 63, rec.nside & ~(1ull << 63), rec.radx, rec.base * radc);
     }
 }
