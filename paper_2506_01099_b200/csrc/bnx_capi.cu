@@ -821,12 +821,13 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     ha.shard = c->shard;
     ha.nshards = c->nshards;
     ha.tail_heavy = c->tail_heavy ? c->tail_heavy : TAIL_HEAVY;
-    // CTAs per SM (measured sweep, scripts/engine_compare.py): one wave of k_heavy_screen
-    // (8 resident CTAs per SM at 32 registers) below ~2^33; more, smaller runs when the sieve
+    // CTAs per SM (measured sweeps, scripts/engine_compare.py, scripts/sweep_time.sh): one
+    // wave of k_heavy_screen below ~2^33 -- 7 CTAs per SM (8 fit at 32 registers, but the
+    // eighth slot left free lets k_heavy_exact's CTAs start early: -1% at 2^32); more, smaller runs when the sieve
     // shares the GPU (40 per SM for domains of 2^38 or more: -2% at 2^40 and 2^44)
     const bool wide_sieve = ha.kmin != ~0ull && !heavy_sieve_mask((int)np2);
     const int grid_mult = c->heavy_grid ? c->heavy_grid
-                                        : (!wide_sieve ? 8 : (n_last - n_first >= (1ull << 38) ? 40 : 20));
+                                        : (!wide_sieve ? 7 : (n_last - n_first >= (1ull << 38) ? 40 : 20));
     const int grid = c->num_sms * grid_mult;
     // k_heavy_exact: a thread per survivor from P2 on (measured: 0.45 ms at 2^40 against
     // 1.17 ms for a warp per survivor trying only the deciding primes, whose per-survivor set-up
