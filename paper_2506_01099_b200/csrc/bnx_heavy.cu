@@ -366,13 +366,15 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
 // takes one and runs the y tests, so the expensive part always runs with full warps.
 __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) {
     constexpr int T = HEAVY_THREADS;
-    // np2 (inv, lim), np2p (inv32, lim32), np2 p, np2p 2^32 mod p (np2p: np2 padded to 32)
-    extern __shared__ ulonglong2 s_il[];
+    // np2p (inv32, lim32) first -- the hot table at a fixed shared address, so the unrolled
+    // mask loop addresses it by immediates -- then np2 (inv, lim), np2 p, np2p 2^32 mod p,
+    // np2p (2^32 mod p) p^-1 mod 2^32 (np2p: np2 padded to 32)
+    extern __shared__ uint2 s_pd32[];
     const int np2p = (a.np2 + 31) & ~31;
-    uint2* s_pd32 = reinterpret_cast<uint2*>(s_il + a.np2);
-    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_pd32 + np2p);
+    ulonglong2* s_il = reinterpret_cast<ulonglong2*>(s_pd32 + np2p);  // (np2p * 8 B: 16-byte aligned)
+    uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + a.np2);
     uint32_t* s_c32 = s_p + a.np2;
-    uint32_t* s_e32 = s_c32 + np2p;  // (2^32 mod p) p^-1 mod 2^32
+    uint32_t* s_e32 = s_c32 + np2p;
     __shared__ HeavyItem s_q[2 * T];
     __shared__ uint64_t s_end[T];  // class ends of a multi-class window
     __shared__ int s_cnt;
@@ -911,12 +913,12 @@ __device__ __forceinline__ void exact_emit(const HeavyArgs& a, bool sideL, uint6
 }
 
 __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
-    // np3 (inv, lim), np3p (inv32, lim32), np3 p, np3p e = (2^32 mod p) p^-1 mod 2^32 (np3p:
-    // np3 padded to 32)
-    extern __shared__ ulonglong2 s_il3[];
+    // np3p (inv32, lim32) first (a fixed shared address: immediate offsets in the unrolled
+    // loops), np3 (inv, lim), np3 p, np3p e = (2^32 mod p) p^-1 mod 2^32 (np3p: np3 padded to 32)
+    extern __shared__ uint2 s_pd3[];
     const int np3 = (int)a.np3, np3p = (np3 + 31) & ~31;
-    uint2* s_pd3 = reinterpret_cast<uint2*>(s_il3 + np3);
-    uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_pd3 + np3p);
+    ulonglong2* s_il3 = reinterpret_cast<ulonglong2*>(s_pd3 + np3p);
+    uint32_t* s_p3 = reinterpret_cast<uint32_t*>(s_il3 + np3);
     uint32_t* s_c3 = s_p3 + np3;
     for (int j = threadIdx.x; j < np3; j += blockDim.x) {
         s_il3[j] = make_ulonglong2(a.pdiv[j].inv, a.pdiv[j].lim);
