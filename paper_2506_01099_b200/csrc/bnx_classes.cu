@@ -75,6 +75,7 @@ __device__ __forceinline__ int factor_tab(uint32_t x, const uint32_t* __restrict
     int n = 0;
     while (x > 1) {
         const uint32_t t = tab[x];
+        BNX_CHECK(n < CLS_MAXD);
         if (!(t & CLS_COMPOSITE)) {  // x is prime
             idx[n] = t;
             ex[n] = 1;
@@ -166,6 +167,7 @@ __global__ void k_cls_build(ClsBuildArgs a) {
             }
             const uint64_t code = cmax - ((uint64_t)j * 64 + e);
             const int w = d / a.dpw, pos = a.dpw - 1 - d % a.dpw;  // most significant first
+            BNX_CHECK(w < a.nwords && w < CLS_MAXW && e < 64);
             words[w] |= code << (pos * a.bits);
             ++d;
         }

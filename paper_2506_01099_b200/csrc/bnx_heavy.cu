@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
                         i = first_class_above(a.incl, cls0 + T - 1, a.nent, w);
                     }
                 }
+                BNX_CHECK(i < a.nent);
                 const BnxHeavyEnt e = a.ent[i];
                 // item -> k: the class's listed k (see wheel_k)
                 const uint64_t k = wheel_k(a.klo[i] + (w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0)), e.rmask & 3u);
@@ -473,6 +474,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
                     if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
                     if (canon) {
                         const int slot = atomicAdd(&s_cnt, 1);
+                        BNX_CHECK(slot < 2 * T);
                         s_q[slot] = HeavyItem{k * e.b, e.m * e.r, k * e.r};
                     }
                 } else {
@@ -575,6 +577,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
                 // can be sparse among the trial classes, so no linear probe from the last one)
                 const uint64_t cls = first_class_above_warp<true>(a.incl, a.nent, ch, tid);
                 if (tid == 0) {
+                    BNX_CHECK(cls < a.nent);
                     const uint64_t first = cls ? a.incl[cls - 1] >> 40 : 0;
                     s_e = a.ent[cls];
                     s_k0 = (ch - first) * (uint64_t)kc;  // index of the chunk's first listed k
@@ -624,6 +627,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
         for (int t = tid; t < a.ntasks; t += blockDim.x) {
             const uint32_t tk = s_task[t];
             const int j = tk & 0x3FF, side = (tk >> 10) & 1;
+            BNX_CHECK(j < np2);
             const uint32_t r = (tk >> 11) & 0x3FF, R = tk >> 21;
             const int32_t off = s_off[2 * j + side];
             if (off < 0) continue;
@@ -649,7 +653,11 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
             }
             bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
             if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
-            if (canon) s_list[atomicAdd(&s_nl, 1)] = (uint32_t)kk;
+            if (canon) {
+                const int li = atomicAdd(&s_nl, 1);
+                BNX_CHECK(li < kc);
+                s_list[li] = (uint32_t)kk;
+            }
         }
         __syncthreads();
         // 4. exact small factors of both sides, then the stage-1 test

@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
             for (uint32_t i = tid; i < nh; i += THREADS) {
                 const uint64_t e = gb[i];
                 const uint32_t o = (uint32_t)e, t = o / TILE, loc = o % TILE;
+                BNX_CHECK(o < SEG);
                 uint32_t k = atomicAdd(&bcnt[t], 1u);
                 if (k < BCAP) bent[t * BCAP + k] = ((e >> 32) << 16) | loc; else a.flags[0] = 1;
             }
@@ -663,8 +664,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sieve_exact(SieveArgs a) {
             // per-tile progressions: balanced work items (see k_screen), exact division per hit
             const int it_end = (int)s_item[warp + 1];
             for (int it = (int)s_item[warp]; it < it_end; ++it) {
+                BNX_CHECK(NW + 1 + it < 2 * MAXS);
                 const uint32_t e = s_item[NW + 1 + it];
                 const int j = (int)(e & 0xFFu);
+                BNX_CHECK(j < nsmall || (e >> 31));
                 if (e >> 31) {
                     const int jj = j + lane;
                     if (jj < nsmall) {
@@ -1171,6 +1174,7 @@ __global__ void k_sieve_buckets(SieveArgs a, uint64_t seg_len, uint64_t* gbuck, 
         const BnxProg pr = a.large[j];
         for (uint64_t o = bnx_first_offset(a.start, pr.q, pr.recip); o < a.length; o += pr.q) {
             const uint64_t seg = o / seg_len;
+            BNX_CHECK(seg < (a.length + seg_len - 1) / seg_len);
             const uint32_t k = atomicAdd(&gcnt[seg], 1u);
             if (k < gcap) gbuck[seg * gcap + k] = ((uint64_t)pr.p << 32) | (o - seg * seg_len);
             else a.flags[3] = 1;

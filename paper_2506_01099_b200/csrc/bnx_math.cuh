@@ -10,6 +10,24 @@
 #define BNX_HD __host__ __device__ __forceinline__
 #define BNX_D __device__ __forceinline__
 
+// Device bounds checks of the checked build (make EXTRA=-DBNX_CHECKED; compute-sanitizer is
+// not available on the GPU pool): a failed check prints its site and traps the kernel.
+#ifdef BNX_CHECKED
+#include <cstdio>
+#define BNX_CHECK(c)                                                                           \
+    do {                                                                                       \
+        if (!(c)) {                                                                            \
+            printf("BNX_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                         \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define BNX_CHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 // Inverse of odd a modulo 2^64 (Newton: 3 -> 6 -> 12 -> 24 -> 48 -> 96 correct bits).
 BNX_HD uint64_t bnx_inv64(uint64_t a) {
     uint64_t x = a;
