@@ -201,6 +201,7 @@ struct bnx_ctx {
     int sieve_nv = 0;              // 32-bit-slot geometry for windows below 2^32 (BNX_SIEVE_NARROW; -1: off)
     int sieve_narrow_blocks_per_sm = 1;
     bool sieve_gbuckets = true;    // large progressions bucketed per window (BNX_SIEVE_GBUCKETS=0: per-segment scan)
+    uint32_t sieve_gcap = 0;       // test only (BNX_SIEVE_GCAP): bucket capacity per segment; 0 = SEG / 128
     DBuf<uint64_t> sieve_gbuck;
     DBuf<uint32_t> sieve_gcnt;
     DBuf<unsigned long long> t_split;
@@ -1241,6 +1242,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sieve_narrow_blocks_per_sm, sv.fn, sv.threads, sv.smem));
     }
     if (const char* env = std::getenv("BNX_SIEVE_GBUCKETS")) c->sieve_gbuckets = std::atoi(env) != 0;
+    if (const char* env = std::getenv("BNX_SIEVE_GCAP")) c->sieve_gcap = (uint32_t)std::max(0, std::atoi(env));
     c->sieve_blocks_per_sm = std::max(1, c->sieve_blocks_per_sm);
     c->sieve_narrow_blocks_per_sm = std::max(1, c->sieve_narrow_blocks_per_sm);
     *out = c;
@@ -1422,7 +1424,7 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
     // global buckets for the large progressions: SEG / 128 entries per segment, ~2.8x the
     // expected hits (the sum over q >= the tile of SEG / q is below SEG / 350); a full one
     // re-runs the call with the per-segment scan
-    const uint32_t gcap = (uint32_t)(SEG / 128);
+    const uint32_t gcap = c->sieve_gcap ? c->sieve_gcap : (uint32_t)(SEG / 128);
     const uint64_t nseg_max = (piece + SEG - 1) / SEG;
     if (gbuckets) {
         TRY(c->sieve_gcnt.ensure(nseg_max));

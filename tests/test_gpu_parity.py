@@ -123,6 +123,22 @@ def test_sieve_global_buckets_vs_oracle(orc, monkeypatch, gbuckets):
         ctx.close()
 
 
+def test_sieve_global_bucket_overflow_falls_back(orc, monkeypatch):
+    """A global bucket that fills up (BNX_SIEVE_GCAP=1 forces it) makes the call re-run with
+    the per-segment scan: same radicals as the oracle."""
+    from paper_2506_01099_b200 import _native
+
+    monkeypatch.setenv("BNX_SIEVE_GCAP", "1")
+    ctx = _native.Context(0)
+    try:
+        for start, length in [(2**40 - 2**20, 2**21 + 3), (2**33 + 5, 3 * 2**19)]:
+            got = ctx.sieve_radicals(start, length, None, 0, True)
+            want = orc.sieve_segment(start, length, orc.primes_up_to(math.isqrt(start + length) + 1), True)
+            assert np.array_equal(got, want), (start, length)
+    finally:
+        ctx.close()
+
+
 # ---------------------------------------------------------------- trial division ---------
 def test_trial_division_vectors(golden):
     for rec in golden["trial_division"]:
