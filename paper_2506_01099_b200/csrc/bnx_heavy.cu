@@ -445,17 +445,22 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
             const uint64_t cls0 = s_cls;
             // class of each item: the whole window in class cls0 (most windows), else the
             // ends of the next T classes staged in shared memory and searched there
-            const bool one = (a.incl[cls0] & HEAVY_TRIAL_MASK) >= min(base + T, b1);  // CTA-uniform
+            const uint64_t wend = min(base + T, b1);  // the window's end
+            const bool one = (a.incl[cls0] & HEAVY_TRIAL_MASK) >= wend;  // CTA-uniform
+            int kwin = T - 1;  // every item of the window lies in staged classes [0, kwin] (or beyond T - 1)
             if (!one) {
                 const uint64_t j = cls0 + tid;
-                s_end[tid] = j < a.nent ? (a.incl[j] & HEAVY_TRIAL_MASK) : ~0ull;
-                __syncthreads();
+                const uint64_t end = j < a.nent ? (a.incl[j] & HEAVY_TRIAL_MASK) : ~0ull;
+                s_end[tid] = end;
+                // the ends are ascending: the classes ending at or after the window's end are
+                // the last `count` staged ones, so the first of them closes the search range
+                kwin = min(T - 1, T - __syncthreads_count(end >= wend));
             }
             uint64_t i = cls0;
             if (w < b1) {
                 if (!one) {
                     if (w < s_end[T - 1]) {
-                        int lo = 0, hi = T - 1;  // first staged class ending above w
+                        int lo = 0, hi = kwin;  // first staged class ending above w
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
                             if (s_end[mid] > w) hi = mid; else lo = mid + 1;
