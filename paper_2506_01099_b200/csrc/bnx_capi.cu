@@ -230,6 +230,7 @@ struct bnx_ctx {
     int heavy_kc = 0;         // tuning only (BNX_HEAVY_KC, k per sieve chunk, multiple of 8); 0 = default
     int sieve_grid = 0;       // tuning only (BNX_SIEVE_GRID, k_heavy_sieve CTAs per SM); 0 = default
     int sieve_threads = 0;    // tuning only (BNX_SIEVE_THREADS, k_heavy_sieve CTA size, 64..256); 0 = default
+    int probe_walk = 0;       // profiling only (BNX_PROBE_WALK)
     int exact_warp = -1;      // tuning only (BNX_EXACT_WARP: 1 warp / 0 thread per survivor); -1 = by bound
     uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
@@ -834,6 +835,7 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // 1.17 ms for a warp per survivor trying only the deciding primes, whose per-survivor set-up
     // outweighs the primes it skips); the warp form serves domains with few survivors
     ha.exact_warp = c->exact_warp >= 0 ? c->exact_warp : 0;
+    ha.probe_walk = c->probe_walk;
     // (measured, scripts/sweep_sieve40.sh: 256-thread CTAs with kc = 768 beat 128 and 64 at
     // 2^40 and 1.4e12 by 6-28%)
     ha.sieve_threads = (uint32_t)c->sieve_threads;
@@ -1209,6 +1211,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_HEAVY_KC")) c->heavy_kc = std::max(0, std::atoi(env)) & ~7;
     if (const char* env = std::getenv("BNX_SIEVE_GRID")) c->sieve_grid = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_SIEVE_THREADS")) c->sieve_threads = std::min(256, std::max(0, std::atoi(env)) & ~31);
+    if (const char* env = std::getenv("BNX_PROBE_WALK")) c->probe_walk = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_EXACT_WARP")) c->exact_warp = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_PAIR_PREFIX"))
         c->pair_prefix = std::min<uint64_t>(PAIR_PREFIX, (uint64_t)std::max(0, std::atoi(env)));

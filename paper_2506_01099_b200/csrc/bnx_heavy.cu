@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         }
         if (cnt == 0) break;
         const int take = min(cnt, T);
-        if (tid < take) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p, s_pd32, s_c32, s_e32);
+        if (tid < take && !a.probe_walk) y_tests(a, s_q[cnt - 1 - tid], s_il, s_p, s_pd32, s_c32, s_e32);
         cnt -= take;
         __syncthreads();
         if (tid == 0) s_cnt = cnt;
@@ -1012,6 +1012,7 @@ cudaError_t heavy_configure() {
         e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_heavy_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+
     cudaFuncAttributes at;  // (the attribute calls above load those three; see kernels_preload)
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, k_heavy_count);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, k_pdiv32);

@@ -121,6 +121,7 @@ struct HeavyArgs {
     uint32_t sieve_ctas;      // k_heavy_sieve grid (0: the screen's)
     uint32_t sieve_threads;   // k_heavy_sieve CTA size (0: 256)
     int exact_warp;           // k_heavy_exact: one warp per survivor, cut prime ranges (else one thread each)
+    int probe_walk;           // profiling only (BNX_PROBE_WALK=1): k_heavy_screen walks and queues, no y tests
 };
 size_t heavy_scan_temp_bytes(uint64_t nent);
 void launch_pdiv32(const BnxPDiv* pdiv, uint64_t n, uint4* out, cudaStream_t st);
