@@ -484,8 +484,11 @@ def run_ours(args) -> None:
             b_ev.synchronize()
             fills.append(a_ev.elapsed_time(b_ev))
         write_peak = 8 * n_sieve / (min(fills[1:]) / 1e3) / 1e9
-        high = {}  # the same 2^30 integers far above 2^32 (u64 slots, huge progressions bucketed per window)
-        for name, st in (("2^40", 1 << 40), ("2^62", 1 << 62)):
+        # the SURVEY 8(d) sieve windows above 2^32 (u64 slots, huge progressions bucketed per
+        # window), and one at 2^62
+        high = {}
+        for name, st in (("2^32", 1 << 32), ("2^40-2^30", (1 << 40) - n_sieve),
+                         ("1.4e12-2^30", 1_400_000_000_000 - n_sieve), ("2^62", 1 << 62)):
             ctx.sieve_radicals_dev(st, n_sieve, out.data_ptr())  # warm-up: tables
             ts = []
             for k in range(3):
