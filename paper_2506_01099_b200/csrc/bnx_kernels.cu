@@ -1220,8 +1220,12 @@ void launch_sieve_pipe(const SieveArgs& a, int grid, cudaStream_t st) {
     SieveVariant{T, N, H, B, (const void*)k_sieve_exact<T, N, H, B, SIEVE_MAXS, M, A>, sieve_smem<T, N, B, A>(), \
                  launch_sieve_v<T, N, H, B, M, A>}
 static const SieveVariant kSieveVariants[] = {
-    // default; the others measured slower on [1, 2^30] (scripts/sieve_variants.py,
-    // profiles/r01_sieve_variants.jsonl): 2.18 ms against 2.44, 2.62, 2.78
+    // u64 slots (windows reaching 2^32; below, kSieveNarrow).  Default: 6144-slot tiles (48 KB),
+    // 384 threads, three CTAs per SM -- 2^30 integers at 2^40 in 2.03 ms against 2.19 ms for
+    // the round-1 geometry (index 1: 8192 slots, 512 threads, two CTAs per SM), 2.08-2.63 ms for
+    // the other tile sizes and CTA shapes tried (profiles/r02_sieve_windows.jsonl); identical
+    // output hashes
+    BNX_SIEVE_VARIANT(6144, 32, 384, 64, 3, false),
     BNX_SIEVE_VARIANT(SIEVE_TILE, SIEVE_NT, SIEVE_THREADS, SIEVE_BCAP, 2, false),
     BNX_SIEVE_VARIANT(8192, 64, 768, 64, 2, false),
     BNX_SIEVE_VARIANT(8192, 64, 256, 64, 4, false),
@@ -1233,9 +1237,11 @@ static const SieveVariant kSieveVariants[] = {
     BNX_SIEVE_VARIANT(8192, 64, 512, 64, 1, true),
     // the barrier-free pipeline (k_sieve_pipe): 16 compute warps + a store warp, one CTA per
     // SM (three 64 KB tiles): no barrier stalls, but too few warps to hide the shared-memory
-    // CAS latency (3.84 ms on [1, 2^30] against 2.17 ms for variant 0)
+    // CAS latency (3.84 ms on [1, 2^30] against 2.17 ms for the round-1 default)
     SieveVariant{8192, 24, 512, 64, (const void*)k_sieve_pipe<8192, 24, 16, 64, SIEVE_MAXS>,
                  sieve_pipe_smem<8192, 24, 16, 64>(), launch_sieve_pipe<8192, 24, 16, 64>},
+    BNX_SIEVE_VARIANT(6144, 32, 320, 64, 3, false),
+    BNX_SIEVE_VARIANT(6144, 16, 384, 64, 3, false),
 };
 int sieve_variant_count() { return (int)(sizeof(kSieveVariants) / sizeof(kSieveVariants[0])); }
 const SieveVariant& sieve_variant(int i) { return kSieveVariants[i]; }
