@@ -1434,17 +1434,19 @@ static int sieve_common(bnx_ctx* c, uint64_t start, uint64_t length, const uint6
         TRY(c->sieve_gbuck.ensure(nseg_max * gcap));
         Tables& t = c->sieve_tab;
         if (!t.split && t.nlarge) {  // medium progressions to the front, huge ones to the back (once per table)
-            DBuf<BnxProg> tmp;
-            TRY(tmp.ensure(t.nlarge));
+            struct Scratch {  // (released on every path out)
+                DBuf<BnxProg> b;
+                ~Scratch() { b.release(); }
+            } tmp;
+            TRY(tmp.b.ensure(t.nlarge));
             TRY(c->t_split.ensure(2));
             CK(cudaMemsetAsync(c->t_split.p, 0, 2 * sizeof(unsigned long long), c->stream));
-            launch_split_large(t.large.p, t.nlarge, tmp.p, c->t_split.p, c->stream);
+            launch_split_large(t.large.p, t.nlarge, tmp.b.p, c->t_split.p, c->stream);
             CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(t.large.p, tmp.p, sizeof(BnxProg) * t.nlarge, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(t.large.p, tmp.b.p, sizeof(BnxProg) * t.nlarge, cudaMemcpyDeviceToDevice, c->stream));
             unsigned long long nm = 0;
             CK(cudaMemcpyAsync(&nm, c->t_split.p, sizeof(nm), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
-            tmp.release();
             t.nmedium = nm;
             t.split = true;
         } else if (!t.nlarge) {
