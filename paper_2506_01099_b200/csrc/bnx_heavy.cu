@@ -767,11 +767,13 @@ __device__ __forceinline__ void emit_candidate(const HeavyArgs& a, const BnxCand
 template <bool NARROW>
 __device__ __forceinline__ uint64_t rad_cofactor_thread(uint64_t o, int j_first, int np3, const ulonglong2* s_il3,
                                                         const uint2* s_pd3, const uint32_t* s_p3, const uint32_t* s_e3,
-                                                        bool nowrap = false) {
+                                                        bool nowrap = false, uint32_t top = 0xFFFFFFFFu) {
     using W = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     W c = (W)o, rad = 1;
     const uint32_t ol = (uint32_t)o, oh = (uint32_t)(o >> 32);
-    for (int j0 = j_first; j0 < np3; j0 += 32) {
+    // blocks up to the first prime above `top` (>= cbrt of every cofactor of the warp: beyond
+    // it at most two prime factors remain, settled by the square test below)
+    for (int j0 = j_first; j0 < np3 && s_p3[j0] <= top; j0 += 32) {
         const int jn = min(32, np3 - j0);
         uint32_t m = 0;
         if constexpr (NARROW) {
@@ -968,17 +970,45 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         return;
     }
     const int j_first = np2 & ~31;  // (a block boundary: the primes below np2 no longer divide)
+    // Each CTA takes 256 survivors at a time and sorts them by cofactor size (five bins, a
+    // counting sort in shared memory), so that a warp's cofactors are alike: the 32-bit form
+    // for whole warps below 2^32, and the trial division stops at the warp's largest cube root.
+    __shared__ uint32_t s_srt[256];  // survivor indices (the records are re-read: L1/L2 hits)
+    __shared__ int s_bcnt[5], s_boff[5];
     for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < nq; i0 += nthreads) {
         const uint64_t i = i0 + threadIdx.x;
         const bool live = i < nq;
-        const BnxSurv rec = live ? a.q1[i] : BnxSurv{0, 1, 1, 1};
+        BnxSurv rec = live ? a.q1[i] : BnxSurv{0, 1, 1, 1};
+        uint32_t top = 0xFFFFFFFFu;
+        if (np3 > 320) {  // (short prime tables -- bounds below ~2^33 -- gain nothing from it)
+            const int lg = 63 - __clzll(rec.c | 1);
+            const int bin = lg < 32 ? 0 : min(4, (lg - 32) / 2 + 1);
+            if (threadIdx.x < 5) s_bcnt[threadIdx.x] = 0;
+            __syncthreads();
+            const int pos = live ? atomicAdd(&s_bcnt[bin], 1) : 0;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int o = 0;
+                for (int b = 0; b < 5; ++b) {
+                    s_boff[b] = o;
+                    o += s_bcnt[b];
+                }
+            }
+            __syncthreads();
+            if (live) s_srt[s_boff[bin] + pos] = (uint32_t)threadIdx.x;
+            __syncthreads();
+            rec = live ? a.q1[i0 + s_srt[threadIdx.x]] : BnxSurv{0, 1, 1, 1};  // (the live ones fill the front)
+            top = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)approx_cbrt((float)rec.c) + 2u);
+            __syncthreads();  // (s_srt is refilled next round)
+        }
         // 32-bit arithmetic when every cofactor of the warp fits (mixed warps would run both);
         // above, the one-step reduction when no cofactor of the warp can wrap
         const uint64_t radc =
             __all_sync(0xFFFFFFFFu, rec.c < (1ull << 32))
-                ? rad_cofactor_thread<true>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3)
+                ? rad_cofactor_thread<true>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3, false, top)
                 : rad_cofactor_thread<false>(rec.c, j_first, np3, s_il3, s_pd3, s_p3, s_c3,
-                                             __all_sync(0xFFFFFFFFu, (rec.c & 0xFFFFFFFFull) + (rec.c >> 32) * pmax < (1ull << 32)));
+                                             __all_sync(0xFFFFFFFFu, (rec.c & 0xFFFFFFFFull) + (rec.c >> 32) * pmax < (1ull << 32)),
+                                             top);
         if (live) exact_emit(a, rec.nside >> 63, rec.nside & ~(1ull << 63), rec.radx, rec.base * radc);
     }
 }
@@ -1008,8 +1038,13 @@ cudaError_t heavy_configure() {
     cudaError_t e = cudaFuncSetAttribute(k_heavy_sieve<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_heavy_sieve<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) {  // (227 KB per block in all, its static shared memory included)
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, k_heavy_exact);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_heavy_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024 - (int)fa.sharedSizeBytes);
+    }
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_heavy_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
 
