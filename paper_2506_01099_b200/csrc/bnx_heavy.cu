@@ -970,11 +970,12 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         return;
     }
     const int j_first = np2 & ~31;  // (a block boundary: the primes below np2 no longer divide)
-    // Each CTA takes 256 survivors at a time and sorts them by cofactor size (five bins, a
+    // Each CTA takes 256 survivors at a time and sorts them by cofactor size (bins by powers of two, a
     // counting sort in shared memory), so that a warp's cofactors are alike: the 32-bit form
     // for whole warps below 2^32, and the trial division stops at the warp's largest cube root.
     __shared__ uint32_t s_srt[256];  // survivor indices (the records are re-read: L1/L2 hits)
-    __shared__ int s_bcnt[5], s_boff[5];
+    constexpr int NBIN = 18;  // 0: below 2^32, then one per power of two up to 2^48
+    __shared__ int s_bcnt[NBIN], s_boff[NBIN];
     for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < nq; i0 += nthreads) {
         const uint64_t i = i0 + threadIdx.x;
         const bool live = i < nq;
@@ -982,14 +983,14 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         uint32_t top = 0xFFFFFFFFu;
         if (np3 > 320) {  // (short prime tables -- bounds below ~2^33 -- gain nothing from it)
             const int lg = 63 - __clzll(rec.c | 1);
-            const int bin = lg < 32 ? 0 : min(4, (lg - 32) / 2 + 1);
-            if (threadIdx.x < 5) s_bcnt[threadIdx.x] = 0;
+            const int bin = lg < 32 ? 0 : min(NBIN - 1, lg - 31);
+            if (threadIdx.x < NBIN) s_bcnt[threadIdx.x] = 0;
             __syncthreads();
             const int pos = live ? atomicAdd(&s_bcnt[bin], 1) : 0;
             __syncthreads();
             if (threadIdx.x == 0) {
                 int o = 0;
-                for (int b = 0; b < 5; ++b) {
+                for (int b = 0; b < NBIN; ++b) {
                     s_boff[b] = o;
                     o += s_bcnt[b];
                 }
