@@ -970,20 +970,38 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
         return;
     }
     const int j_first = np2 & ~31;  // (a block boundary: the primes below np2 no longer divide)
-    // Each CTA takes 256 survivors at a time and sorts them by cofactor size (bins by powers of two, a
+    // Each CTA takes 256 survivors at a time and sorts them by the last prime they need (bins by powers of two, a
     // counting sort in shared memory), so that a warp's cofactors are alike: the 32-bit form
     // for whole warps below 2^32, and the trial division stops at the warp's largest cube root.
     __shared__ uint32_t s_srt[256];  // survivor indices (the records are re-read: L1/L2 hits)
-    constexpr int NBIN = 18;  // 0: below 2^32, then one per power of two up to 2^48
+    constexpr int NBIN = 18;  // by the bit length of the last prime needed (below 2^17)
     __shared__ int s_bcnt[NBIN], s_boff[NBIN];
     for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < nq; i0 += nthreads) {
         const uint64_t i = i0 + threadIdx.x;
         const bool live = i < nq;
         BnxSurv rec = live ? a.q1[i] : BnxSurv{0, 1, 1, 1};
         uint32_t top = 0xFFFFFFFFu;
+        // The last prime the trial division needs: cbrt(c) (beyond it at most two prime
+        // factors remain); or, when the survivor can only pass through a p^2 q factor with
+        // p >= tau' = max(tau, p1) > cbrt(c) (tau = c rad x base / 2n, as in
+        // rad_cofactor_warp), only q <= c / tau'^2 -- a q found is divided off, a c left
+        // unfactored is taken squarefree, which then fails the exact test as it must (cubes,
+        // whose s = p^2 may pass, keep the full range).
+        auto need_of = [&](const BnxSurv& r) -> uint32_t {
+            const float cf = (float)r.c;
+            const uint32_t t3 = (uint32_t)approx_cbrt(cf) + 2u;
+            const uint64_t n = r.nside & ~(1ull << 63);
+            const float tau = cf * (float)r.radx * (float)r.base / (2.0f * (float)n) * 0.9999f;
+            const float tp = fmaxf(tau, (float)a.p1);
+            if (tp <= (float)t3) return t3;
+            const uint64_t cr = (uint64_t)rintf(approx_cbrt(cf));
+            if (cr * cr * cr == r.c) return t3;
+            const float hb = cf / (tp * tp) * 1.0001f + 2.0f;
+            return hb < (float)t3 ? (uint32_t)hb : t3;
+        };
         if (np3 > 320) {  // (short prime tables -- bounds below ~2^33 -- gain nothing from it)
-            const int lg = 63 - __clzll(rec.c | 1);
-            const int bin = lg < 32 ? 0 : min(NBIN - 1, lg - 31);
+            const uint32_t nd = need_of(rec);
+            const int bin = min(NBIN - 1, 32 - __clz(nd));
             if (threadIdx.x < NBIN) s_bcnt[threadIdx.x] = 0;
             __syncthreads();
             const int pos = live ? atomicAdd(&s_bcnt[bin], 1) : 0;
@@ -999,7 +1017,7 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
             if (live) s_srt[s_boff[bin] + pos] = (uint32_t)threadIdx.x;
             __syncthreads();
             rec = live ? a.q1[i0 + s_srt[threadIdx.x]] : BnxSurv{0, 1, 1, 1};  // (the live ones fill the front)
-            top = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)approx_cbrt((float)rec.c) + 2u);
+            top = __reduce_max_sync(0xFFFFFFFFu, need_of(rec));
             __syncthreads();  // (s_srt is refilled next round)
         }
         // 32-bit arithmetic when every cofactor of the warp fits (mixed warps would run both);

@@ -101,6 +101,10 @@ def main():
                 stats["cut"] += 1
                 tp = max(t, p1)
                 top = icbrt(c)
+                if tp > top:
+                    stats["tau_above_cbrt"] = stats.get("tau_above_cbrt", 0) + 1
+                    hb = min(top, c // (tp * tp))
+                    stats["sum_ratio_hiB_top"] = stats.get("sum_ratio_hiB_top", 0.0) + hb / top
                 lo_b, hi_b = p1, min(top, c // (tp * tp))
                 lo_a, hi_a = tp, top - 1
                 # 32-prime blocks (from index np2) a lane needs
