@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(256) k_heavy_exact(HeavyArgs a) {
             const float hb = cf / (tp * tp) * 1.0001f + 2.0f;
             return hb < (float)t3 ? (uint32_t)hb : t3;
         };
-        if (np3 > 320) {  // (short prime tables -- bounds below ~2^33 -- gain nothing from it)
+        if (np3 > 128) {  // (short prime tables gain nothing from it)
             const uint32_t nd = need_of(rec);
             const int bin = min(NBIN - 1, 32 - __clz(nd));
             if (threadIdx.x < NBIN) s_bcnt[threadIdx.x] = 0;
