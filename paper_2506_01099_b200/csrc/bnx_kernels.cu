@@ -400,13 +400,64 @@ struct TailCand {
     uint64_t n, r0, r1, R, s0, s1, t0, t1;
 };
 
+// n + 1 < 2^32: every cofactor is below 2^32 (the products t r1, t r0 of the second kind
+// too: t r0 = m / r1 + s1 < 2 (n + 1) / r1 with r1 >= 2), so they are formed mod 2^32 and
+// tested with 32-bit Montgomery products; m itself (t R can pass 2^32) in 64 bits.
+__device__ __forceinline__ TailCand tail_cand(uint64_t n, uint64_t r0, uint64_t r1, unsigned kinds) {
+    TailCand c;
+    c.n = n; c.r0 = r0; c.r1 = r1; c.R = r0 * r1;
+    if (n + 1 < (1ull << 32)) {
+        const uint32_t n32 = (uint32_t)n;
+        c.s0 = n32 / (uint32_t)r0;
+        c.s1 = (n32 + 1u) / (uint32_t)r1;
+        if (c.R >> 32) {  // R > n + 1
+            c.t1 = 0;
+            c.t0 = 1;
+        } else {
+            const uint32_t R32 = (uint32_t)c.R;
+            c.t1 = (kinds & 1u) ? (n32 - 1u) / R32 : 0;
+            c.t0 = (n32 + 1u) / R32 + 1;
+        }
+    } else {
+        c.s0 = n / r0; c.s1 = (n + 1) / r1;
+        c.t1 = (kinds & 1u) ? (n - 1) / c.R : 0;          // m = n - tR >= 1
+        c.t0 = (n + 1) / c.R + 1;                          // n + 2 <= tR <= 2n
+    }
+    return c;
+}
+__device__ __forceinline__ uint64_t tail_total(const TailCand& c, unsigned kinds) {
+    // second kind: t0 <= t <= floor(2n / R)
+    uint64_t t2;
+    if (c.n + 1 < (1ull << 32) && (c.R >> 32)) {  // R > n: the quotient is 0 or 1
+        t2 = 2 * c.n >= c.R;
+    } else if (c.n + 1 < (1ull << 32)) {  // floor(2n / R) = 2q + [2 (n mod R) >= R], q = n / R
+        const uint32_t n32 = (uint32_t)c.n, R32 = (uint32_t)c.R, q = n32 / R32;
+        t2 = 2ull * q + (2ull * (n32 - q * R32) >= R32);
+    } else {
+        t2 = (2 * c.n) / c.R;
+    }
+    return c.t1 + (((kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0);
+}
+
 __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_begin, uint64_t k_end) {
     const int lane = threadIdx.x & 31;
+    const bool narrow = c.n + 1 < (1ull << 32);
     for (uint64_t base = k_begin; base < k_end; base += 32) {
         const uint64_t k = base + lane;
         uint64_t m = 0;
         bool ok = false;
-        if (k < k_end) {
+        if (k < k_end && narrow) {
+            const uint32_t r0 = (uint32_t)c.r0, r1 = (uint32_t)c.r1, s0 = (uint32_t)c.s0, s1 = (uint32_t)c.s1;
+            if (k < c.t1) {
+                const uint32_t t = (uint32_t)k + 1u;
+                m = c.n - (uint64_t)t * c.R;
+                ok = bnx_supported_by32(s0 - t * r1, r0) && bnx_supported_by32(s1 - t * r0, r1);
+            } else {
+                const uint32_t t = (uint32_t)(c.t0 + (k - c.t1));
+                m = (uint64_t)t * c.R - c.n - 1;
+                ok = bnx_supported_by32(t * r0 - s1, r1) && bnx_supported_by32(t * r1 - s0, r0);
+            }
+        } else if (k < k_end) {
             if (k < c.t1) {
                 const uint64_t t = k + 1;
                 m = c.n - t * c.R;
@@ -467,14 +518,8 @@ __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
             rad2_warp(n, a.pdiv, a.npdiv, r0, r1);
             if (__umul64hi(r0, r1) != 0 || r0 * r1 > 2 * n) continue;  // warp-uniform
         }
-        TailCand c;
-        c.n = n; c.r0 = r0; c.r1 = r1; c.R = r0 * r1;
-        c.s0 = n / r0; c.s1 = (n + 1) / r1;
-        c.t1 = (a.kinds & 1u) ? (n - 1) / c.R : 0;          // m = n - tR >= 1
-        c.t0 = (n + 1) / c.R + 1;                            // n + 2 <= tR <= 2n
-        const uint64_t t2 = (2 * n) / c.R;
-        const uint64_t c2 = ((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0;
-        const uint64_t total = c.t1 + c2;
+        const TailCand c = tail_cand(n, r0, r1, a.kinds);
+        const uint64_t total = tail_total(c, a.kinds);
         if (lane == 0 && !a.cands) {  // (heavy engine: counted and routed by k_heavy_exact)
             atomicAdd(&a.ctr[CTR_CAND], 1ull);
             if (total) atomicAdd(&a.ctr[CTR_CHECKS], (unsigned long long)total);
@@ -501,13 +546,8 @@ __global__ void __launch_bounds__(256) k_tail_heavy(TailArgs a) {
     const uint64_t nh = min((uint64_t)a.ctr[CTR_HEAVY], a.heavy_cap);
     for (uint64_t y = blockIdx.y; y < nh; y += gridDim.y) {
         const BnxCand h = a.heavy[y];
-        TailCand c;
-        c.n = h.n; c.r0 = h.r0; c.r1 = h.r1; c.R = h.r0 * h.r1;
-        c.s0 = h.n / h.r0; c.s1 = (h.n + 1) / h.r1;
-        c.t1 = (a.kinds & 1u) ? (h.n - 1) / c.R : 0;
-        c.t0 = (h.n + 1) / c.R + 1;
-        const uint64_t t2 = (2 * h.n) / c.R;
-        const uint64_t total = c.t1 + (((a.kinds & 2u) && t2 >= c.t0) ? t2 - c.t0 + 1 : 0);
+        const TailCand c = tail_cand(h.n, h.r0, h.r1, a.kinds);
+        const uint64_t total = tail_total(c, a.kinds);
         const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
         for (uint64_t chunk = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); chunk * 32 < total;
              chunk += nwarps)

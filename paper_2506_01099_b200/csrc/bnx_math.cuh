@@ -86,6 +86,30 @@ BNX_D bool bnx_supported_by(uint64_t u, uint64_t r) {
     return twos_ok && (u == 1 || x == 0);
 }
 
+// The same below 2^32 (u, r < 2^32): 32-bit Montgomery products, a quarter of the multiplies.
+BNX_D uint32_t bnx_redc32(uint32_t hi, uint32_t lo, uint32_t u, uint32_t nu) {  // (hi:lo) 2^-32 mod u
+    const uint32_t m = lo * nu;                                                 // nu = -u^-1 mod 2^32
+    const uint64_t t = (uint64_t)hi + __umulhi(m, u) + (lo != 0);               // < 2u
+    return (uint32_t)(t >= u ? t - u : t);
+}
+
+BNX_D bool bnx_supported_by32(uint32_t u, uint32_t r) {
+    const int tz = __ffs(u) - 1;
+    const bool twos_ok = tz == 0 || (r & 1) == 0;
+    u >>= tz;
+    uint32_t v = u;  // u^-1 mod 2^32 (3 correct bits, doubled by each step)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v *= 2u - u * v;
+    const uint32_t nu = 0u - v;
+    uint32_t x = bnx_redc32(0, r, u, nu);  // r 2^-32 mod u
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const uint64_t s = (uint64_t)x * x;
+        x = bnx_redc32((uint32_t)(s >> 32), (uint32_t)s, u, nu);
+    }
+    return twos_ok && (u == 1 || x == 0);
+}
+
 // floor(4 * log2(v)) for v >= 1, exact: 4e + #{k in 1..3 : mantissa >= 2^(k/4)}.
 // The constants are ceil(2^(63 + k/4)), computed with integer roots.
 BNX_D int bnx_floor4log2(uint64_t v) {
