@@ -14,3 +14,4 @@ timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__b
 timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r2_heavy_launches_2p40.csv python scripts/profile_search.py 40 1 > /dev/null 2>&1; echo ncu40 rc=$?
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_bench_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-sieve --no-2p40 > /dev/null 2>&1; echo ncubench rc=$?
 timeout 600 python scripts/paper_range.py > gpurun_out/r2_paper_range.jsonl 2> gpurun_out/r2_paper_range.err; echo range rc=$?
+timeout 300 ncu --set full --clock-control none --import-source on -k k_tail -c 1 -o gpurun_out/r2_k_tail python scripts/profile_search.py 32 > gpurun_out/r2_ncu_tail.log 2>&1; echo ncutail rc=$?
