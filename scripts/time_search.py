@@ -52,6 +52,6 @@ for d in args.domains:
         kt.append(ctx.kernel_timing())
     ctx.set_timing(0)
     st = ctx.stats()
-    print(json.dumps({"tag": args.tag, "lo": lo, "hi": hi, "pairs": len(rows), "median_ms": statistics.median(ms),
+    print(json.dumps({"tag": args.tag, "lo": lo, "hi": hi, "pairs": len(rows), "median_ms": statistics.median(ms), "mean_ms": statistics.fmean(ms),
                       "min_ms": min(ms), "kernels_ms": {k: round(statistics.median(x[k] for x in kt), 4) for k in kt[0]},
                       "survivors": st["survivors"], "candidates": st["candidates"]}), flush=True)
