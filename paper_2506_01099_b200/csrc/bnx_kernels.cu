@@ -400,23 +400,25 @@ struct TailCand {
     uint64_t n, r0, r1, R, s0, s1, t0, t1;
 };
 
-// n + 1 < 2^32: every cofactor is below 2^32 (the products t r1, t r0 of the second kind
-// too: t r0 = m / r1 + s1 < 2 (n + 1) / r1 with r1 >= 2), so they are formed mod 2^32 and
-// tested with 32-bit Montgomery products; m itself (t R can pass 2^32) in 64 bits.
+// n < 2^32 (n + 1 <= 2^32): every cofactor is below 2^32 (the products t r1, t r0 of the
+// second kind too: t r0 = m / r1 + s1 < 2 (n + 1) / r1 <= 2^32 with r1 >= 2), so they are
+// formed mod 2^32 and tested with 32-bit Montgomery products; m itself (t R can pass 2^32) in
+// 64 bits.  The quotients of n + 1 (which may be 2^32) come from those of n: r1 | n + 1
+// gives (n + 1) / r1 = n / r1 + 1, and (n + 1) / R = q + [r + 1 = R] for n = q R + r.
 __device__ __forceinline__ TailCand tail_cand(uint64_t n, uint64_t r0, uint64_t r1, unsigned kinds) {
     TailCand c;
     c.n = n; c.r0 = r0; c.r1 = r1; c.R = r0 * r1;
-    if (n + 1 < (1ull << 32)) {
+    if (n < (1ull << 32)) {
         const uint32_t n32 = (uint32_t)n;
         c.s0 = n32 / (uint32_t)r0;
-        c.s1 = (n32 + 1u) / (uint32_t)r1;
-        if (c.R >> 32) {  // R > n + 1
+        c.s1 = n32 / (uint32_t)r1 + 1u;
+        if (c.R >> 32) {  // R >= 2^32 >= n + 1
             c.t1 = 0;
-            c.t0 = 1;
+            c.t0 = (n + 1 == c.R) + 1;
         } else {
-            const uint32_t R32 = (uint32_t)c.R;
+            const uint32_t R32 = (uint32_t)c.R, q = n32 / R32, r = n32 - q * R32;
             c.t1 = (kinds & 1u) ? (n32 - 1u) / R32 : 0;
-            c.t0 = (n32 + 1u) / R32 + 1;
+            c.t0 = (uint64_t)q + (r + 1u == R32) + 1;
         }
     } else {
         c.s0 = n / r0; c.s1 = (n + 1) / r1;
@@ -428,9 +430,10 @@ __device__ __forceinline__ TailCand tail_cand(uint64_t n, uint64_t r0, uint64_t 
 __device__ __forceinline__ uint64_t tail_total(const TailCand& c, unsigned kinds) {
     // second kind: t0 <= t <= floor(2n / R)
     uint64_t t2;
-    if (c.n + 1 < (1ull << 32) && (c.R >> 32)) {  // R > n: the quotient is 0 or 1
+    const bool narrow = c.n < (1ull << 32);
+    if (narrow && (c.R >> 32)) {  // R > n: the quotient is 0 or 1
         t2 = 2 * c.n >= c.R;
-    } else if (c.n + 1 < (1ull << 32)) {  // floor(2n / R) = 2q + [2 (n mod R) >= R], q = n / R
+    } else if (narrow) {  // floor(2n / R) = 2q + [2 (n mod R) >= R], q = n / R
         const uint32_t n32 = (uint32_t)c.n, R32 = (uint32_t)c.R, q = n32 / R32;
         t2 = 2ull * q + (2ull * (n32 - q * R32) >= R32);
     } else {
@@ -441,7 +444,7 @@ __device__ __forceinline__ uint64_t tail_total(const TailCand& c, unsigned kinds
 
 __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_begin, uint64_t k_end) {
     const int lane = threadIdx.x & 31;
-    const bool narrow = c.n + 1 < (1ull << 32);
+    const bool narrow = c.n < (1ull << 32);
     for (uint64_t base = k_begin; base < k_end; base += 32) {
         const uint64_t k = base + lane;
         uint64_t m = 0;
@@ -487,7 +490,6 @@ __device__ void tail_members(const TailArgs& a, const TailCand& c, uint64_t k_be
         }
     }
 }
-
 
 __global__ void __launch_bounds__(256) k_tail(TailArgs a) {
     // (a programmatic dependent launch: wait for the producer grid's completion and flush;
