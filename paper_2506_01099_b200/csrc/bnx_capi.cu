@@ -119,7 +119,7 @@ struct HeavyTab {
     uint64_t nent = 0;
     DBuf<uint32_t> kinfo;
     uint64_t nkinfo = 0;
-    DBuf<uint64_t> cnt, incl;
+    DBuf<uint64_t> cnt, incl, tile_tot;
     DBuf<uint32_t> klo, kcnt;
     DBuf<uint32_t> tasks;  // k_heavy_sieve marking tasks for (tasks_np2, tasks_kc)
     DBuf<uint16_t> invtab;  // inverses mod p of the primes <= P2 (k_heavy_sieve)
@@ -151,6 +151,7 @@ struct HeavyTab {
         kinfo.release();
         cnt.release();
         incl.release();
+        tile_tot.release();
         klo.release();
         kcnt.release();
         tasks.release();
@@ -231,6 +232,7 @@ struct bnx_ctx {
     int sieve_grid = 0;       // tuning only (BNX_SIEVE_GRID, k_heavy_sieve CTAs per SM); 0 = default
     int sieve_threads = 0;    // tuning only (BNX_SIEVE_THREADS, k_heavy_sieve CTA size, 64..256); 0 = default
     int probe_walk = 0;       // profiling only (BNX_PROBE_WALK)
+    int local_scan = 1;       // tuning only (BNX_LOCAL_SCAN=0: the cub scan at every bound)
     int exact_warp = -1;      // tuning only (BNX_EXACT_WARP: 1 warp / 0 thread per survivor); -1 = by bound
     uint64_t tail_heavy = 0;  // tuning only (BNX_TAIL_HEAVY); 0 = TAIL_HEAVY
     uint32_t shard = 0, nshards = 1;  // bnx_ctx_set_shard
@@ -596,6 +598,7 @@ int build_heavy(bnx_ctx* c, uint64_t max_x) {
     tr.mark("classes: build + sort");
     h.release_build();  // (stream-ordered: the per-search buffers below reuse the memory)
     TRY(h.cnt.ensure(total));
+    TRY(h.tile_tot.ensure((total + HEAVY_TILE - 1) / HEAVY_TILE));
     TRY(h.incl.ensure(total));
     TRY(h.klo.ensure(total));
     TRY(h.kcnt.ensure(total));
@@ -660,6 +663,7 @@ int build_heavy_host(bnx_ctx* c, uint64_t max_x) {
     TRY(h.ent.ensure(ents.size()));
     TRY(h.kinfo.ensure(K));
     TRY(h.cnt.ensure(ents.size()));
+    TRY(h.tile_tot.ensure((ents.size() + HEAVY_TILE - 1) / HEAVY_TILE));
     TRY(h.incl.ensure(ents.size()));
     TRY(h.klo.ensure(ents.size()));
     TRY(h.kcnt.ensure(ents.size()));
@@ -836,6 +840,14 @@ int enqueue_heavy(bnx_ctx* c, uint64_t n_first, uint64_t n_last, uint32_t kinds)
     // outweighs the primes it skips); the warp form serves domains with few survivors
     ha.exact_warp = c->exact_warp >= 0 ? c->exact_warp : 0;
     ha.probe_walk = c->probe_walk;
+    {  // no sieve classes and few tiles: per-tile count scan, the tile offsets scanned by the
+        // screen itself (no scan kernels between the count and the screen)
+        const uint64_t nt = (h.nent + HEAVY_TILE - 1) / HEAVY_TILE;
+        if (c->local_scan && ha.kmin == ~0ull && nt && nt <= (uint64_t)HEAVY_TILES_MAX) {
+            ha.ntiles = (uint32_t)nt;
+            ha.tile_tot = h.tile_tot.p;
+        }
+    }
     // (measured, scripts/sweep_sieve40.sh: 256-thread CTAs with kc = 768 beat 128 and 64 at
     // 2^40 and 1.4e12 by 6-28%)
     ha.sieve_threads = (uint32_t)c->sieve_threads;
@@ -1212,6 +1224,7 @@ int bnx_ctx_create(int device, bnx_ctx_t** out) {
     if (const char* env = std::getenv("BNX_SIEVE_GRID")) c->sieve_grid = std::max(0, std::atoi(env));
     if (const char* env = std::getenv("BNX_SIEVE_THREADS")) c->sieve_threads = std::min(256, std::max(0, std::atoi(env)) & ~31);
     if (const char* env = std::getenv("BNX_PROBE_WALK")) c->probe_walk = std::atoi(env) != 0;
+    if (const char* env = std::getenv("BNX_LOCAL_SCAN")) c->local_scan = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_EXACT_WARP")) c->exact_warp = std::atoi(env) != 0;
     if (const char* env = std::getenv("BNX_PAIR_PREFIX"))
         c->pair_prefix = std::min<uint64_t>(PAIR_PREFIX, (uint64_t)std::max(0, std::atoi(env)));

@@ -154,63 +154,105 @@ __device__ __forceinline__ uint64_t wheel_k(uint64_t rho, uint32_t wsel) {
     }
 }
 
+// The packed item count of class i (trial items in the low 40 bits, sieve chunks above): the
+// k range [ceil(x_lo / b), min(2m, floor(x_hi / b))] of the domain; also the class's first
+// listed k / item rank (klo) and, for a sieve class, its number of listed k (kcnt).
+__device__ __forceinline__ uint64_t class_count(const HeavyArgs& a, uint64_t i) {
+    const BnxHeavyEnt e = a.ent[i];
+    uint64_t kh = 2 * e.m;
+    uint64_t kl = 1;
+    if (e.b > a.x_hi) {
+        kh = 0;
+    } else {
+        // floor(x_hi / b) and ceil(x_lo / b): a double estimate, corrected in integers
+        const double rb = 1.0 / (double)e.b;
+        uint64_t top = (uint64_t)((double)a.x_hi * rb);
+        while (top * e.b > a.x_hi) --top;
+        while ((top + 1) * e.b <= a.x_hi) ++top;
+        if (top < kh) kh = top;
+        if (a.x_lo > e.b) {  // (else ceil(x_lo / b) = 1: every search from n = 1)
+            uint64_t lo = (uint64_t)((double)a.x_lo * rb);
+            while (lo > 0 && lo * e.b >= a.x_lo) --lo;
+            while (lo * e.b < a.x_lo) ++lo;  // smallest lo with lo * b >= x_lo
+            if (lo > kl) kl = lo;
+        }
+    }
+    const uint64_t c = kh >= kl ? kh - kl + 1 : 0;
+    if (c >= a.kmin) {  // sieve chunks over every k (every odd k when sigma is even)
+        const uint64_t st = (e.rmask & 1u) ? 2 : 1;
+        const uint64_t ks = st == 2 ? (kl | 1u) : kl;
+        const uint64_t cs = kh >= ks ? (kh - ks) / st + 1 : 0;
+        a.klo[i] = (uint32_t)ks;
+        a.kcnt[i] = (uint32_t)cs;  // listed k (index space)
+        return ((cs + a.kc - 1) / a.kc) << 40;
+    }
+    // trial items: the k coprime to 2 and 3 where sigma has them (wheel_k)
+    const uint32_t wsel = e.rmask & 3u;
+    const uint64_t r0 = wheel_rank(kl - 1, wsel);
+    a.klo[i] = (uint32_t)r0;  // rank of the class's first item
+    a.kcnt[i] = 0;            // (sieve classes only)
+    return c ? wheel_rank(kh, wsel) - r0 : 0;
+}
+
 __global__ void k_heavy_count(HeavyArgs a) {
     // the search's counters and flags start here (no memset launches; every later kernel
     // runs after this one)
     if (blockIdx.x == 0 && threadIdx.x < CTR_N) a.ctr[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x < 4) a.flags[threadIdx.x] = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.nent;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const BnxHeavyEnt e = a.ent[i];
-        uint64_t kh = 2 * e.m;
-        uint64_t kl = 1;
-        if (e.b > a.x_hi) {
-            kh = 0;
-        } else {
-            // floor(x_hi / b) and ceil(x_lo / b): a double estimate, corrected in integers
-            const double rb = 1.0 / (double)e.b;
-            uint64_t top = (uint64_t)((double)a.x_hi * rb);
-            while (top * e.b > a.x_hi) --top;
-            while ((top + 1) * e.b <= a.x_hi) ++top;
-            if (top < kh) kh = top;
-            if (a.x_lo > e.b) {  // (else ceil(x_lo / b) = 1: every search from n = 1)
-                uint64_t lo = (uint64_t)((double)a.x_lo * rb);
-                while (lo > 0 && lo * e.b >= a.x_lo) --lo;
-                while (lo * e.b < a.x_lo) ++lo;  // smallest lo with lo * b >= x_lo
-                if (lo > kl) kl = lo;
-            }
-        }
-        const uint64_t c = kh >= kl ? kh - kl + 1 : 0;
-        if (c >= a.kmin) {  // sieve chunks over every k (every odd k when sigma is even)
-            const uint64_t st = (e.rmask & 1u) ? 2 : 1;
-            const uint64_t ks = st == 2 ? (kl | 1u) : kl;
-            const uint64_t cs = kh >= ks ? (kh - ks) / st + 1 : 0;
-            a.cnt[i] = ((cs + a.kc - 1) / a.kc) << 40;
-            a.klo[i] = (uint32_t)ks;
-            a.kcnt[i] = (uint32_t)cs;  // listed k (index space)
-            continue;
-        } else {  // trial items: the k coprime to 2 and 3 where sigma has them (wheel_k)
-            const uint32_t wsel = e.rmask & 3u;
-            const uint64_t r0 = wheel_rank(kl - 1, wsel);
-            a.cnt[i] = c ? wheel_rank(kh, wsel) - r0 : 0;
-            a.klo[i] = (uint32_t)r0;  // rank of the class's first item
-        }
-        a.kcnt[i] = 0;  // (sieve classes only)
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a.cnt[i] = class_count(a, i);
+}
+
+// Inclusive scan of the values of one block of 256 threads (every thread gets its own).
+__device__ __forceinline__ uint64_t block_scan256(uint64_t v, uint64_t* s_w, uint64_t& total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+        if (lane >= d) x += y;
     }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    uint64_t pre = 0;
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint64_t t = s_w[w];
+        pre += w < wid ? t : 0;
+        total += t;
+    }
+    return pre + x;
+}
+
+// Few classes and no sieve classes (bounds below ~2^33): the counts scanned per tile of
+// HEAVY_TILE classes only -- incl holds the prefix within the tile, tile_tot the tile totals,
+// which k_heavy_screen scans for itself in its prologue (no scan kernels between the count
+// and the screen).
+__global__ void __launch_bounds__(HEAVY_TILE) k_heavy_count_local(HeavyArgs a) {
+    if (blockIdx.x == 0 && threadIdx.x < CTR_N) a.ctr[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 4) a.flags[threadIdx.x] = 0;
+    __shared__ uint64_t s_w[8];
+    const uint64_t i = (uint64_t)blockIdx.x * HEAVY_TILE + threadIdx.x;
+    uint64_t total;
+    const uint64_t x = block_scan256(i < a.nent ? class_count(a, i) : 0, s_w, total);
+    if (i < a.nent) a.incl[i] = x;
+    if (threadIdx.x == 0) a.tile_tot[blockIdx.x] = total;
 }
 
 // Class of item w: smallest i >= lo with incl[i] > w (galloping, then binary search).
-__device__ __forceinline__ uint64_t first_class_above(const uint64_t* __restrict__ incl, uint64_t lo, uint64_t n,
-                                                      uint64_t w) {
+template <class Incl>
+__device__ __forceinline__ uint64_t first_class_above(const Incl& incl, uint64_t lo, uint64_t n, uint64_t w) {
     uint64_t step = 1, hi = lo;
-    while (hi < n - 1 && (incl[hi] & HEAVY_TRIAL_MASK) <= w) {
+    while (hi < n - 1 && (incl(hi) & HEAVY_TRIAL_MASK) <= w) {
         lo = hi + 1;
         hi = min(n - 1, hi + step);
         step <<= 1;
     }
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
-        if ((incl[mid] & HEAVY_TRIAL_MASK) > w) hi = mid; else lo = mid + 1;
+        if ((incl(mid) & HEAVY_TRIAL_MASK) > w) hi = mid; else lo = mid + 1;
     }
     return lo;
 }
@@ -218,13 +260,12 @@ __device__ __forceinline__ uint64_t first_class_above(const uint64_t* __restrict
 // The same search by a whole warp: 32 probes per round narrow [lo, hi] 32-fold, so a run's
 // first class costs ~4 dependent L2 loads instead of ~2 log2(nent) (requires w < incl[n-1]).
 // CHUNKS: search the sieve-chunk prefix (incl >> 40) instead of the trial-item prefix.
-template <bool CHUNKS = false>
-__device__ __forceinline__ uint64_t first_class_above_warp(const uint64_t* __restrict__ incl, uint64_t n,
-                                                           uint64_t w, int lane) {
+template <bool CHUNKS = false, class Incl>
+__device__ __forceinline__ uint64_t first_class_above_warp(const Incl& incl, uint64_t n, uint64_t w, int lane) {
     uint64_t lo = 0, hi = n - 1;  // the answer lies in [lo, hi]
     while (lo < hi) {
         const uint64_t span = hi - lo;
-        const uint64_t v = incl[lo + span * (lane + 1) / 32];
+        const uint64_t v = incl(lo + span * (lane + 1) / 32);
         const bool above = (CHUNKS ? v >> 40 : v & HEAVY_TRIAL_MASK) > w;
         const int j = __ffs(__ballot_sync(0xFFFFFFFFu, above)) - 1;  // lane 31 probes hi: j >= 0
         const uint64_t nlo = j ? lo + span * j / 32 + 1 : lo;
@@ -364,6 +405,9 @@ __device__ __forceinline__ void y_tests(const HeavyArgs& a, const HeavyItem& it,
 // takes item base + t: neighbouring k of one class, or neighbouring classes).  Canonical
 // items go to a shared-memory queue; whenever it holds a full CTA's worth, every thread
 // takes one and runs the y tests, so the expensive part always runs with full warps.
+// LOCAL: the class prefix counts come per tile (k_heavy_count_local); the tile offsets are
+// scanned here into shared memory and added on every read.
+template <bool LOCAL>
 __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) {
     constexpr int T = HEAVY_THREADS;
     // np2p (inv32, lim32) first -- the hot table at a fixed shared address, so the unrolled
@@ -375,6 +419,9 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     uint32_t* s_p = reinterpret_cast<uint32_t*>(s_il + a.np2);
     uint32_t* s_c32 = s_p + a.np2;
     uint32_t* s_e32 = s_c32 + np2p;
+    // LOCAL: ntiles tile offsets (8-byte aligned: the tables above end 4 bytes short of it when
+    // np2 is odd)
+    uint64_t* s_pre = reinterpret_cast<uint64_t*>(s_e32 + np2p + (a.np2 & 1));
     __shared__ HeavyItem s_q[2 * T];
     __shared__ uint64_t s_end[T];  // class ends of a multi-class window
     __shared__ int s_cnt;
@@ -394,6 +441,36 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
         s_e32[j] = 0u;
     }
     if (tid == 0) s_cnt = 0;
+    if constexpr (LOCAL) {  // exclusive scan of the tile totals (each thread a run of tiles)
+        static_assert(T == 256, "block_scan256");
+        const int nt = (int)a.ntiles, per = (nt + T - 1) / T;
+        uint64_t loc = 0;
+        for (int j = 0; j < per; ++j) {
+            const int t = tid * per + j;
+            if (t < nt) {
+                const uint64_t v = a.tile_tot[t];
+                s_pre[t] = v;
+                loc += v;
+            }
+        }
+        __shared__ uint64_t s_w[8];
+        uint64_t total;
+        uint64_t run = block_scan256(loc, s_w, total) - loc;
+        for (int j = 0; j < per; ++j) {
+            const int t = tid * per + j;
+            if (t < nt) {
+                const uint64_t v = s_pre[t];
+                s_pre[t] = run;
+                run += v;
+            }
+        }
+        __syncthreads();
+    }
+    // the global inclusive prefix of class i
+    auto incl = [&](uint64_t i) -> uint64_t {
+        if constexpr (LOCAL) return a.incl[i] + s_pre[i / HEAVY_TILE];
+        else return a.incl[i];
+    };
     // k_heavy_exact may be scheduled now (programmatic dependent launch): its CTAs take the
     // SMs our CTAs leave and stage their prime tables before they wait for our completion
     asm volatile("griddepcontrol.launch_dependents;");
@@ -402,7 +479,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
     // r * nshards + s, so every shard samples the whole class range (the classes differ in
     // canonical density).  CTA g starts with run g and then fetches runs from a counter, so
     // CTAs that drew sparse runs take more of them (the SMs finish together).
-    const uint64_t Wt = a.incl[a.nent - 1] & HEAVY_TRIAL_MASK;
+    const uint64_t Wt = incl(a.nent - 1) & HEAVY_TRIAL_MASK;
     const uint64_t WA = a.run_mult ? Wt * min(a.run_first, 256u) / 256 : Wt;  // items of the static runs
     const uint64_t nr = (uint64_t)gridDim.x * (1 + a.run_mult);
     __shared__ unsigned long long s_run;
@@ -435,7 +512,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
                 }
                 run = ~0ull;
                 if (tid < 32 && base < b1) {
-                    const uint64_t c0 = first_class_above_warp(a.incl, a.nent, base, tid);
+                    const uint64_t c0 = first_class_above_warp(incl, a.nent, base, tid);
                     if (tid == 0) s_cls = c0;
                 }
                 __syncthreads();
@@ -446,11 +523,11 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
             // class of each item: the whole window in class cls0 (most windows), else the
             // ends of the next T classes staged in shared memory and searched there
             const uint64_t wend = min(base + T, b1);  // the window's end
-            const bool one = (a.incl[cls0] & HEAVY_TRIAL_MASK) >= wend;  // CTA-uniform
+            const bool one = (incl(cls0) & HEAVY_TRIAL_MASK) >= wend;  // CTA-uniform
             int kwin = T - 1;  // every item of the window lies in staged classes [0, kwin] (or beyond T - 1)
             if (!one) {
                 const uint64_t j = cls0 + tid;
-                const uint64_t end = j < a.nent ? (a.incl[j] & HEAVY_TRIAL_MASK) : ~0ull;
+                const uint64_t end = j < a.nent ? (incl(j) & HEAVY_TRIAL_MASK) : ~0ull;
                 s_end[tid] = end;
                 // the ends are ascending: the classes ending at or after the window's end are
                 // the last `count` staged ones, so the first of them closes the search range
@@ -467,13 +544,13 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 8) k_heavy_screen(HeavyArgs a) 
                         }
                         i = cls0 + lo;
                     } else {
-                        i = first_class_above(a.incl, cls0 + T - 1, a.nent, w);
+                        i = first_class_above(incl, cls0 + T - 1, a.nent, w);
                     }
                 }
                 BNX_CHECK(i < a.nent);
                 const BnxHeavyEnt e = a.ent[i];
                 // item -> k: the class's listed k (see wheel_k)
-                const uint64_t k = wheel_k(a.klo[i] + (w - (i ? a.incl[i - 1] & HEAVY_TRIAL_MASK : 0)), e.rmask & 3u);
+                const uint64_t k = wheel_k(a.klo[i] + (w - (i ? incl(i - 1) & HEAVY_TRIAL_MASK : 0)), e.rmask & 3u);
                 if (k < a.nkinfo) {
                     bool canon = (a.kinfo[k] & (e.rmask | 0x80000000u)) == 0;
                     if (canon && e.rbig > 1 && k >= e.rbig_min) canon = gcd32((uint32_t)k, e.rbig) == 1;
@@ -580,7 +657,7 @@ __global__ void __launch_bounds__(256) k_heavy_sieve(HeavyArgs a) {
             if (enter) {
                 // the class: first with chunk prefix > ch (a 32-way search: the sieved classes
                 // can be sparse among the trial classes, so no linear probe from the last one)
-                const uint64_t cls = first_class_above_warp<true>(a.incl, a.nent, ch, tid);
+                const uint64_t cls = first_class_above_warp<true>([&](uint64_t j) { return a.incl[j]; }, a.nent, ch, tid);
                 if (tid == 0) {
                     BNX_CHECK(cls < a.nent);
                     const uint64_t first = cls ? a.incl[cls - 1] >> 40 : 0;
@@ -1065,10 +1142,13 @@ cudaError_t heavy_configure() {
                                      227 * 1024 - (int)fa.sharedSizeBytes);
     }
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_heavy_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        e = cudaFuncSetAttribute(k_heavy_screen<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_heavy_screen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
 
     cudaFuncAttributes at;  // (the attribute calls above load those three; see kernels_preload)
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, k_heavy_count);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, k_heavy_count_local);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, k_pdiv32);
     return e;
 }
@@ -1105,10 +1185,14 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
     bool pdl = false;
     if (kev) cudaEventRecord(kev[0], st);
     if (a.nent) {
-        const unsigned cb = (unsigned)std::min<uint64_t>((a.nent + 255) / 256, 4096);
-        k_heavy_count<<<cb, 256, 0, st>>>(a);
-        size_t bytes = scan_temp_bytes;
-        cub::DeviceScan::InclusiveSum(scan_temp, bytes, a.cnt, a.incl, (int64_t)a.nent, st);
+        if (a.ntiles) {
+            k_heavy_count_local<<<a.ntiles, HEAVY_TILE, 0, st>>>(a);
+        } else {
+            const unsigned cb = (unsigned)std::min<uint64_t>((a.nent + 255) / 256, 4096);
+            k_heavy_count<<<cb, 256, 0, st>>>(a);
+            size_t bytes = scan_temp_bytes;
+            cub::DeviceScan::InclusiveSum(scan_temp, bytes, a.cnt, a.incl, (int64_t)a.nent, st);
+        }
         const bool sieve = a.kmin != ~0ull;
         if (sieve) {  // the sieve (shared-memory atomics) runs beside the trial screen (IMAD pipe)
             cudaEventRecord(ev_fork, st);
@@ -1130,7 +1214,10 @@ void launch_heavy(const HeavyArgs& a, void* scan_temp, size_t scan_temp_bytes, i
             if (kev) for (int i = 2; i < 4; ++i) cudaEventRecord(kev[i], st);
             return;
         }
-        k_heavy_screen<<<grid, HEAVY_THREADS, smem2, st>>>(a);
+        if (a.ntiles)
+            k_heavy_screen<true><<<grid, HEAVY_THREADS, smem2 + sizeof(uint64_t) * (a.ntiles + 1), st>>>(a);
+        else
+            k_heavy_screen<false><<<grid, HEAVY_THREADS, smem2, st>>>(a);
         if (sieve) cudaStreamWaitEvent(st, ev_join, 0);
         pdl = !sieve && !kev;
     } else if (kev) {

@@ -71,6 +71,8 @@ struct TailArgs {
 
 // Heavy-side generator (bnx_heavy.cu).
 constexpr int HEAVY_THREADS = 256;
+constexpr int HEAVY_TILE = 256;          // classes per tile of k_heavy_count_local
+constexpr int HEAVY_TILES_MAX = 1024;    // tile offsets staged in k_heavy_screen's shared memory (8 KB)
 constexpr int HEAVY_NP2 = 1023;  // odd primes <= y_max^(1/4) staged in shared memory (10-bit task index)
 constexpr int HEAVY_NP3 = 7000;  // odd primes <= cbrt(y_max) staged in shared memory (S <= 2^48)
 // Classes with at least HEAVY_KMIN values of k in a domain are sieved over k (k_heavy_sieve)
@@ -84,7 +86,9 @@ struct HeavyArgs {
     const BnxHeavyEnt* ent;
     uint64_t nent;
     uint64_t* cnt;    // per class: number of k in the domain
-    uint64_t* incl;   // inclusive scan of cnt
+    uint64_t* incl;   // inclusive scan of cnt (ntiles > 0: within each tile of HEAVY_TILE classes)
+    uint64_t* tile_tot;  // ntiles > 0: the tiles' totals (k_heavy_count_local)
+    uint32_t ntiles;     // > 0: per-tile scan, the screen adds the tile offsets (no sieve classes)
     uint32_t* klo;    // per class: first k in the domain
     uint32_t* kcnt;   // per class: number of k in the domain
     const uint32_t* tasks;  // sieve marking tasks: j | side << 10 | r << 11 | R << 21

@@ -512,3 +512,28 @@ def test_exact_stage_modes(orc, monkeypatch, mode):
         assert ctx.stats()["candidates"] == 2253
     finally:
         ctx.close()
+
+
+@pytest.mark.gpu
+def test_local_tile_scan_matches_cub_scan(monkeypatch):
+    """Below ~2^33 (no sieve classes) the class counts are scanned per tile of 256 and the
+    screen adds the tile offsets itself; BNX_LOCAL_SCAN=0 keeps the cub scan.  Same rows and
+    counters either way, from bounds with an odd number of stage-1 primes up to 2^32."""
+    from paper_2506_01099_b200 import _native
+
+    base = _native.context(0)
+    monkeypatch.setenv("BNX_LOCAL_SCAN", "0")
+    ctx = _native.Context(0)
+    try:
+        keys = ("survivors", "candidates", "residue_checks", "matches", "pairs")
+        for lo, hi in [(1, 1000), (1, 2**20), (3, 2**26 + 12345), (2**31 - 2**22, 2**31 + 2**22),
+                       (2**32 - 2**21, 2**32 - 1), (1, 2**32 - 1), (5, 2**33)]:
+            for kinds in (1, 3):
+                a = base.search_domain(lo, hi, kinds, None, 0)
+                sa = base.stats()
+                b = ctx.search_domain(lo, hi, kinds, None, 0)
+                sb = ctx.stats()
+                assert a.tobytes() == b.tobytes(), (lo, hi, kinds)
+                assert {k: sa[k] for k in keys} == {k: sb[k] for k in keys}, (lo, hi, kinds)
+    finally:
+        ctx.close()
